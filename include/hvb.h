@@ -1,0 +1,129 @@
+/* hvb.h -- C ABI of libhvb.so, the B200 (sm_100a) kernels of the
+ * paper_2003_12663_b200 indirect-BEM drop-in.
+ *
+ * The reference (hvbem 0.1.0, pure Python/NumPy) has no native FFI; its hot
+ * path is the Python call chain listed per entry point below (paths are
+ * relative to reference pkg/src/hvbem/).  The drop-in keeps that Python API
+ * (paper_2003_12663_b200.assembly / solver / postprocess) and routes every
+ * heavy loop through these functions.
+ *
+ * Conventions: all array pointers are DEVICE pointers to caller-owned,
+ * contiguous buffers (PyTorch tensors on the Python side); sizes are element
+ * counts; `stream` is a cudaStream_t; launches are asynchronous.  Return 0
+ * (HVB_OK) or an HVB_E* code; hvb_last_error() returns a thread-local
+ * message.  "Original" collocation columns follow the mesh's collocation
+ * order; "device" columns are the matrix storage order.
+ */
+#ifndef HVB_H_
+#define HVB_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HVB_ABI_VERSION 1
+
+#define HVB_OK 0
+#define HVB_EARG 1    /* invalid argument (maps to ValueError)            */
+#define HVB_ECUDA 2   /* CUDA launch/runtime error (maps to RuntimeError)  */
+
+const char* hvb_last_error(void);
+int hvb_version(void);
+
+/* K1 -- regular-rule sample table: table[t][q] = (y_tq, jw_tq*hat_c(q)/4pi),
+ * 6 doubles per (t,q); rule = nq x (u, v, w, 0).
+ * Replaces: TriangleTables.__init__  assembly.py:78-103 */
+int hvb_build_table(const double* nodes6, int nt, int nq, const double* rule, double* table, void* stream);
+
+/* Pack the per-column-tile panel streams (one record of 6*nq+8 doubles per
+ * (tile, panel) entry): sample table, circumcircle classification bracket
+ * thr = fl(eta*R), owned local columns.  ent_meta = (mfirst, l0, l1, l2,
+ * flags) per entry.  Replaces: the per-row classification setup of
+ * row_pass1  assembly.py:155-168 */
+int hvb_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
+                     const int* ent_meta, long long n_entries, double* stream_out, void* stream);
+
+/* K2+K3 -- regular sweep of n_rows collocation rows against every panel,
+ * classification fused (regular iff ||x-cc|| > eta*R with the reference's
+ * rounding), SL (kind 0) or ADL (kind 1) kernel, each entry written once
+ * as row_scale * sum, for row-list entries [row_begin, row_begin+n_rows).
+ * Non-regular, non-singular pairs are appended to
+ * near_list as (row-list index, triangle).  mode: 0 all-SL, 1 all-ADL,
+ * 2 mixed.  Replaces: row_pass1 regular part  assembly.py:170-200 and
+ * _kernel_values 126-132 */
+int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_col0,
+                         const int* tile_width, int n_tiles, int nq, int row_begin, int n_rows, const double* rowdata,
+                         const int* row_kind, const int* row_col, const double* row_scale,
+                         const long long* row_out, double* A, const int* tri_cols, int mode, int warps_per_block,
+                         int* near_list, unsigned long long* near_count, long long near_cap, void* stream);
+
+/* K4 (+K6 diagonal) -- singular corner pairs with the split-corner Duffy
+ * rule (3 x n_rule x 4 table), then A[row, own] += row_diag.
+ * Replaces: row_pass1 singular batch  assembly.py:202-235; dielectric
+ * diagonal _row_equation 436-437 */
+int hvb_assemble_singular(const double* nodes6, const int* tri_cols, const int* col_dev, const int* vc_ptr,
+                          const int* vc_tri, const int* vc_corner, const double* rule, int n_rule, int n_rows,
+                          const double* rowdata, const int* row_kind, const int* row_col, const double* row_scale,
+                          const double* row_diag, const long long* row_out, double* A, void* stream);
+
+/* K6 -- floating-potential columns n..n+n_fl-1 of collocation rows (-1 in
+ * the row's own floating column).  Replaces: _row_equation 425-426 */
+int hvb_fill_float_cols(double* A, const long long* row_out, const int* row_float, int n_rows, int n, int n_fl,
+                        void* stream);
+
+/* K5 -- deferred near-singular pairs: closest point, subdivision, graded
+ * composite rule, kernel (kind 0 SL, 1 ADL, 2 E, 3 potential); writes 9
+ * corner contributions per pair.  Replaces: row_pass2  assembly.py:245-292,
+ * near_singular_rule  quadrature.py:409-450 */
+int hvb_near_pairs(const int* pairs, long long n_pairs, const double* points, const int* kind,
+                   const double* nodes6, const double* radii, const double* duffy, int n_duffy,
+                   const double* graded, int n_graded, int bisect_depth, double bisect_trigger, double* out,
+                   void* stream);
+
+/* add sorted near-pair contributions to matrix rows (deterministic order) */
+int hvb_near_apply_rows(const int* seg_ptr, int n_seg, const int* pairs, const double* contrib,
+                        const int* tri_cols, const int* col_dev, const double* row_scale, const long long* row_out,
+                        double* A, void* stream);
+
+/* K8 -- y = left .* (A xp), A row-major (lda % 4 == 0), f64 or f32 storage.
+ * Replaces: matvec  assembly.py:376-400 (inside solver op, solver.py:116-118) */
+int hvb_gemv(const void* A, int is_f32, long long lda, int n_rows, int n_cols, const double* x, const double* left,
+             double* y, void* stream);
+
+/* xp[k] = z[perm[k]] / right[perm[k]]  (perm/right may be NULL) */
+int hvb_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp, void* stream);
+
+/* K9 -- row max |a_ij| and diagonal.  Replaces: solver.py:98-107,
+ * SystemMatrix.diagonal assembly.py:348-353 */
+int hvb_rowmax_diag(const void* A, int is_f32, long long lda, int n_rows, int n_cols, const int* diag_col,
+                    double* rowmax, double* diag, void* stream);
+
+/* K10 -- density contraction: src[t][q] = (y_tq, sum_c u_col(t,c) w_c(t,q)) */
+int hvb_contract(const double* table, int nt, int nq, const int* tri_cols, const double* u, double* src,
+                 void* stream);
+
+/* K10/K11 -- N-body potential (potential=1) or field at m points over the
+ * regular panels; panel range split `split` ways into part (split, m, 4);
+ * near pairs appended as (point, triangle).
+ * Replaces: eval_potential / eval_efield  postprocess.py:112-133 */
+int hvb_field(const double* src, const double* cls, const int* tri_cols, int nt, int nq, const double* pts,
+              const int* own_col, int m, int split, int potential, double* part, int* near_list,
+              unsigned long long* near_count, long long near_cap, void* stream);
+
+int hvb_field_reduce(const double* part, int split, int m, double* out, void* stream);
+
+int hvb_near_apply_points(const int* seg_ptr, int n_seg, const int* pairs, const double* contrib,
+                          const int* tri_cols, const double* u, int potential, double* out, void* stream);
+
+/* K11 -- singular star of collocation points with the E kernel, jump term
+ * side*u_i/2*n_i and |E|.  Replaces: surface_field_magnitudes
+ * postprocess.py:141-170 */
+int hvb_field_singular(const double* nodes6, const int* tri_cols, const int* vc_ptr, const int* vc_tri,
+                       const int* vc_corner, const double* rule, int n_rule, const double* pts,
+                       const double* normals, const int* own_col, int m, const double* u, double side,
+                       double* efield, double* emag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HVB_H_ */

@@ -1,0 +1,254 @@
+// K10/K11: potential and field of the solved density at arbitrary points.
+//
+// Reference: eval_potential / eval_efield src/postprocess.py:112-133 build a
+// full (n,) or (n,3) kernel row and contract it with u; surface field
+// 141-170 adds the singular Duffy part and the jump term.  Here the density
+// is contracted once per solution into point sources q_tq = sum_c
+// u_col(t,c) * jw_tq * hat_c(q) / (4 pi) (k_contract), and each target runs
+// an N-body sum over the regular panels (classified exactly like the
+// assembly rows), deferring near-singular panels to near.cu and singular
+// (own-vertex) panels to k_field_singular.  Targets are split over CTAs, the
+// panel range over grid.y; partial sums are reduced in a fixed order.
+#include "launch.cuh"
+
+namespace hvb {
+
+// q_tq from the sample table and u (original collocation order)
+__global__ void k_contract(const double* __restrict__ table, int nt, int nq, const int* __restrict__ tri_cols,
+                           const double* __restrict__ u, double* __restrict__ src) {
+  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nt * nq) return;
+  int t = g / nq;
+  const double* o = table + 6 * (size_t)g;
+  const int* tc = tri_cols + 3 * (size_t)t;
+  double q = o[3] * u[tc[0]] + o[4] * u[tc[1]] + o[5] * u[tc[2]];
+  double* s = src + 4 * (size_t)g;
+  s[0] = o[0];
+  s[1] = o[1];
+  s[2] = o[2];
+  s[3] = q;
+}
+
+
+
+constexpr int FT = 128;   // targets per CTA
+constexpr int FCH = 32;   // panels per shared-memory chunk
+
+template <int NQ, int POT>
+__global__ void __launch_bounds__(FT) k_field(FieldArgs a) {
+  __shared__ double2 s_src[FCH * NQ * 2];
+  __shared__ double s_cls[FCH * 6];
+  __shared__ int s_cols[FCH * 3];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int ti = blockIdx.x * FT + tid;
+  const bool live = ti < a.m;
+  const int tt = live ? ti : a.m - 1;
+  const d3 X = mk3(a.pts[3 * (size_t)tt], a.pts[3 * (size_t)tt + 1], a.pts[3 * (size_t)tt + 2]);
+  const int own = a.own_col ? a.own_col[tt] : -1;
+  const int tb = (int)((long long)a.nt * blockIdx.y / a.split);
+  const int te = (int)((long long)a.nt * (blockIdx.y + 1) / a.split);
+  double ex = 0.0, ey = 0.0, ez = 0.0;
+  for (int c0 = tb; c0 < te; c0 += FCH) {
+    const int cn = min(FCH, te - c0);
+    __syncthreads();
+    const double2* gs = reinterpret_cast<const double2*>(a.src + (size_t)c0 * NQ * 4);
+    for (int k = tid; k < cn * NQ * 2; k += FT) s_src[k] = gs[k];
+    for (int k = tid; k < cn * 6; k += FT) s_cls[k] = a.cls[(size_t)c0 * 6 + k];
+    for (int k = tid; k < cn * 3; k += FT) s_cols[k] = a.tri_cols[(size_t)c0 * 3 + k];
+    __syncthreads();
+    for (int j = 0; j < cn; ++j) {
+      const double* c = s_cls + 6 * j;
+      const bool reg = is_regular(X, mk3(c[0], c[1], c[2]), c[3], c[4], c[5]);
+      double fx = 0.0, fy = 0.0, fz = 0.0;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const double2 p01 = s_src[(j * NQ + q) * 2];
+        const double2 p2q = s_src[(j * NQ + q) * 2 + 1];
+        const double dx = X.x - p01.x, dy = X.y - p01.y, dz = X.z - p2q.x;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        const double ri = rsqrt_full(r2);
+        if (POT) {
+          fx = fma(p2q.y, ri, fx);
+        } else {
+          const double s = p2q.y * (ri * ri * ri);
+          fx = fma(s, dx, fx);
+          fy = fma(s, dy, fy);
+          fz = fma(s, dz, fz);
+        }
+      }
+      if (reg) {
+        ex += fx;
+        ey += fy;
+        ez += fz;
+      }
+      bool emit = false;
+      if (!reg && live) {
+        const int* tc = s_cols + 3 * j;
+        emit = !(own >= 0 && (tc[0] == own || tc[1] == own || tc[2] == own));
+      }
+      const unsigned msk = __ballot_sync(0xffffffffu, emit);
+      if (msk) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(a.near_count, (unsigned long long)__popc(msk));
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (emit) {
+          long long slot = (long long)b + __popc(msk & ((1u << lane) - 1u));
+          if (slot < a.near_cap) {
+            a.near_list[2 * slot] = ti;
+            a.near_list[2 * slot + 1] = c0 + j;
+          }
+        }
+      }
+    }
+  }
+  if (live) {
+    double* o = a.part + ((size_t)blockIdx.y * a.m + ti) * 4;
+    o[0] = ex;
+    o[1] = ey;
+    o[2] = ez;
+    o[3] = 0.0;
+  }
+}
+
+// fixed-order reduction of the panel splits
+__global__ void k_field_reduce(const double* part, int split, int m, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double s0 = 0, s1 = 0, s2 = 0;
+  for (int s = 0; s < split; ++s) {
+    const double* p = part + ((size_t)s * m + i) * 4;
+    s0 += p[0];
+    s1 += p[1];
+    s2 += p[2];
+  }
+  out[3 * (size_t)i] = s0;
+  out[3 * (size_t)i + 1] = s1;
+  out[3 * (size_t)i + 2] = s2;
+}
+
+// near-pair contributions (9 per pair, corner x component) contracted with u
+// and added to the targets in sorted order (one thread per target segment)
+__global__ void k_near_apply_points(const int* seg_ptr, int n_seg, const int* pairs, const double* contrib,
+                                    const int* tri_cols, const double* u, int potential, double* out) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_seg) return;
+  for (int p = seg_ptr[s]; p < seg_ptr[s + 1]; ++p) {
+    const int i = pairs[2 * p], t = pairs[2 * p + 1];
+    const int* tc = tri_cols + 3 * (size_t)t;
+    const double* c = contrib + 9 * (size_t)p;
+    double* o = out + 3 * (size_t)i;
+    if (potential) {
+      o[0] += u[tc[0]] * c[0] + u[tc[1]] * c[1] + u[tc[2]] * c[2];
+    } else {
+      for (int d = 0; d < 3; ++d) o[d] += u[tc[0]] * c[d] + u[tc[1]] * c[3 + d] + u[tc[2]] * c[6 + d];
+    }
+  }
+}
+
+// Surface field at collocation vertices: singular (own star) panels with the
+// corner Duffy rule and the E kernel, contracted with u; then the jump term
+// side * u_i/2 * n_i and |E| (reference src/postprocess.py:152-159).
+__global__ void k_field_singular(const double* nodes6, const int* tri_cols, const int* vc_ptr, const int* vc_tri,
+                                 const int* vc_corner, const double* rule, int nm, const double* pts,
+                                 const double* normals, const int* own_col, int m, const double* u, double side,
+                                 double* efield, double* emag) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= m) return;
+  const int own = own_col[w];
+  const d3 X = mk3(pts[3 * (size_t)w], pts[3 * (size_t)w + 1], pts[3 * (size_t)w + 2]);
+  double* E = efield + 3 * (size_t)w;
+  for (int s = vc_ptr[own]; s < vc_ptr[own + 1]; ++s) {
+    const int t = vc_tri[s], c = vc_corner[s];
+    const double* Xn = nodes6 + 18 * (size_t)t;
+    const double* R = rule + (size_t)c * nm * 4;
+    const int* tc = tri_cols + 3 * (size_t)t;
+    const double u0 = u[tc[0]], u1 = u[tc[1]], u2 = u[tc[2]];
+    double sx = 0, sy = 0, sz = 0;
+    for (int q = lane; q < nm; q += 32) {
+      double uu = R[4 * q], vv = R[4 * q + 1], wq = R[4 * q + 2];
+      d3 p;
+      double jac;
+      curved_point(Xn, uu, vv, p, jac);
+      double dx = X.x - p.x, dy = X.y - p.y, dz = X.z - p.z;
+      double r = sqrt(dx * dx + dy * dy + dz * dz);
+      double sig = u0 * (1.0 - uu - vv) + u1 * uu + u2 * vv;
+      double k = sig * wq * jac * kInv4Pi / (r * r * r);
+      sx = fma(k, dx, sx);
+      sy = fma(k, dy, sy);
+      sz = fma(k, dz, sz);
+    }
+    sx = warp_sum(sx);
+    sy = warp_sum(sy);
+    sz = warp_sum(sz);
+    if (lane == 0) {
+      E[0] += sx;
+      E[1] += sy;
+      E[2] += sz;
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && emag) {
+    const double h = side * 0.5 * u[own];
+    double ex = E[0] + h * normals[3 * (size_t)own];
+    double ey = E[1] + h * normals[3 * (size_t)own + 1];
+    double ez = E[2] + h * normals[3 * (size_t)own + 2];
+    emag[w] = sqrt(ex * ex + ey * ey + ez * ez);
+  }
+}
+
+template <int NQ>
+static cudaError_t launch_field_nq(const FieldArgs& a, cudaStream_t st) {
+  dim3 grid((a.m + FT - 1) / FT, a.split);
+  if (a.potential)
+    k_field<NQ, 1><<<grid, FT, 0, st>>>(a);
+  else
+    k_field<NQ, 0><<<grid, FT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_field(const FieldArgs& a, cudaStream_t st) {
+  if (a.m == 0) return cudaSuccess;
+  switch (a.nq) {
+    case 3: return launch_field_nq<3>(a, st);
+    case 6: return launch_field_nq<6>(a, st);
+    case 12: return launch_field_nq<12>(a, st);
+    case 16: return launch_field_nq<16>(a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_contract(const double* table, int nt, int nq, const int* tri_cols, const double* u, double* src,
+                            cudaStream_t st) {
+  int n = nt * nq;
+  k_contract<<<(n + 255) / 256, 256, 0, st>>>(table, nt, nq, tri_cols, u, src);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_field_reduce(const double* part, int split, int m, double* out, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  k_field_reduce<<<(m + 255) / 256, 256, 0, st>>>(part, split, m, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_near_apply_points(const int* seg_ptr, int n_seg, const int* pairs, const double* contrib,
+                                     const int* tri_cols, const double* u, int potential, double* out,
+                                     cudaStream_t st) {
+  if (n_seg == 0) return cudaSuccess;
+  k_near_apply_points<<<(n_seg + 127) / 128, 128, 0, st>>>(seg_ptr, n_seg, pairs, contrib, tri_cols, u, potential,
+                                                           out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_field_singular(const double* nodes6, const int* tri_cols, const int* vc_ptr, const int* vc_tri,
+                                  const int* vc_corner, const double* rule, int nm, const double* pts,
+                                  const double* normals, const int* own_col, int m, const double* u, double side,
+                                  double* efield, double* emag, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  k_field_singular<<<(m * 32 + 127) / 128, 128, 0, st>>>(nodes6, tri_cols, vc_ptr, vc_tri, vc_corner, rule, nm, pts,
+                                                         normals, own_col, m, u, side, efield, emag);
+  return cudaGetLastError();
+}
+
+}  // namespace hvb

@@ -1,0 +1,184 @@
+// K8/K9: streaming GEMV for the GMRES matvec and the solver's row scans.
+//
+// Reference: matvec src/assembly.py:376-400 (per-row dot), solver row
+// equilibration / diagonal src/solver.py:98-108.
+//
+// y[i] = left[i] * sum_k A[i,k] * xp[k] with A row-major (lda >= N, 16-byte
+// aligned rows) in device column order and xp the (permuted, scaled) Krylov
+// vector.  A CTA owns ROWS rows; every thread loads each 16-byte x chunk
+// once and reuses it for all ROWS rows, so x costs 1/ROWS of the matrix
+// traffic (from L2) and the matrix itself is streamed with evict-first
+// loads.  The per-row summation order depends only on N and the thread
+// count, never on the row blocking: results are bitwise identical for any
+// block partition (reference invariance, tests/test_assembly.py:72-78).
+#include "launch.cuh"
+
+namespace hvb {
+
+constexpr int GEMV_THREADS = 256;
+
+template <int ROWS>
+__global__ void __launch_bounds__(GEMV_THREADS) k_gemv_f64(const double* __restrict__ A, int64_t lda, int nrows,
+                                                           int ncols, const double* __restrict__ x,
+                                                           const double* __restrict__ left,
+                                                           double* __restrict__ y) {
+  const int r0 = blockIdx.x * ROWS;
+  const int tid = threadIdx.x;
+  double acc[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) acc[r] = 0.0;
+  const int n2 = ncols >> 1;
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  const double2* rowp[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    int rr = min(r0 + r, nrows - 1);
+    rowp[r] = reinterpret_cast<const double2*>(A + (int64_t)rr * lda);
+  }
+#pragma unroll 2
+  for (int k = tid; k < n2; k += GEMV_THREADS) {
+    const double2 xv = __ldg(x2 + k);
+    double2 av[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) av[r] = __ldcs(rowp[r] + k);
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) acc[r] = fma(av[r].y, xv.y, fma(av[r].x, xv.x, acc[r]));
+  }
+  if ((ncols & 1) && tid == 0) {
+    const double xv = x[ncols - 1];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      int rr = min(r0 + r, nrows - 1);
+      acc[r] = fma(A[(int64_t)rr * lda + ncols - 1], xv, acc[r]);
+    }
+  }
+  __shared__ double red[ROWS][GEMV_THREADS / 32];
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    double v = warp_sum(acc[r]);
+    if (lane == 0) red[r][wid] = v;
+  }
+  __syncthreads();
+  if (tid < ROWS && r0 + tid < nrows) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < GEMV_THREADS / 32; ++w) s += red[tid][w];
+    y[r0 + tid] = left ? left[r0 + tid] * s : s;
+  }
+}
+
+template <int ROWS>
+__global__ void __launch_bounds__(GEMV_THREADS) k_gemv_f32(const float* __restrict__ A, int64_t lda, int nrows,
+                                                           int ncols, const double* __restrict__ x,
+                                                           const double* __restrict__ left,
+                                                           double* __restrict__ y) {
+  // single-precision storage (reference casts v to float32 and reduces in
+  // float32, src/assembly.py:388); we keep float32 products but reduce in
+  // float64 -- at least as accurate, documented in DESIGN.md.
+  const int r0 = blockIdx.x * ROWS;
+  const int tid = threadIdx.x;
+  double acc[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) acc[r] = 0.0;
+  const int n4 = ncols >> 2;
+  const float4* rowp[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    int rr = min(r0 + r, nrows - 1);
+    rowp[r] = reinterpret_cast<const float4*>(A + (int64_t)rr * lda);
+  }
+  for (int k = tid; k < n4; k += GEMV_THREADS) {
+    const float x0 = (float)x[4 * k], x1 = (float)x[4 * k + 1], x2 = (float)x[4 * k + 2], x3 = (float)x[4 * k + 3];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      float4 a = __ldcs(rowp[r] + k);
+      acc[r] += (double)(a.x * x0) + (double)(a.y * x1) + (double)(a.z * x2) + (double)(a.w * x3);
+    }
+  }
+  if (tid == 0) {
+    for (int c = n4 * 4; c < ncols; ++c) {
+      const float xv = (float)x[c];
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) {
+        int rr = min(r0 + r, nrows - 1);
+        acc[r] += (double)(A[(int64_t)rr * lda + c] * xv);
+      }
+    }
+  }
+  __shared__ double red[ROWS][GEMV_THREADS / 32];
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    double v = warp_sum(acc[r]);
+    if (lane == 0) red[r][wid] = v;
+  }
+  __syncthreads();
+  if (tid < ROWS && r0 + tid < nrows) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < GEMV_THREADS / 32; ++w) s += red[tid][w];
+    y[r0 + tid] = left ? left[r0 + tid] * s : s;
+  }
+}
+
+// xp[k] = z[perm[k]] / right[perm[k]]   (right may be null)
+__global__ void k_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  int j = perm ? perm[k] : k;
+  double v = z[j];
+  xp[k] = right ? v / right[j] : v;
+}
+
+// per-row max |A[i,:]| and the diagonal A[i, diag_col[i]]
+template <typename T>
+__global__ void k_rowmax_diag(const T* A, int64_t lda, int nrows, int ncols, const int* diag_col,
+                              double* rowmax, double* diag) {
+  const int r = blockIdx.x;
+  if (r >= nrows) return;
+  const T* row = A + (int64_t)r * lda;
+  double m = 0.0;
+  for (int k = threadIdx.x; k < ncols; k += blockDim.x) m = fmax(m, fabs((double)row[k]));
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = fmax(mm, red[w]);
+    rowmax[r] = mm;
+    if (diag) diag[r] = diag_col[r] >= 0 ? (double)row[diag_col[r]] : 0.0;
+  }
+}
+
+cudaError_t launch_gemv(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const double* x,
+                        const double* left, double* y, cudaStream_t st) {
+  if (nrows == 0) return cudaSuccess;
+  constexpr int R = 8;
+  dim3 grid((nrows + R - 1) / R);
+  if (is_f32)
+    k_gemv_f32<R><<<grid, GEMV_THREADS, 0, st>>>((const float*)A, lda, nrows, ncols, x, left, y);
+  else
+    k_gemv_f64<R><<<grid, GEMV_THREADS, 0, st>>>((const double*)A, lda, nrows, ncols, x, left, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp,
+                                cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_gather_scale<<<(n + 255) / 256, 256, 0, st>>>(z, right, perm, n, xp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rowmax_diag(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const int* diag_col,
+                               double* rowmax, double* diag, cudaStream_t st) {
+  if (nrows == 0) return cudaSuccess;
+  if (is_f32)
+    k_rowmax_diag<float><<<nrows, 256, 0, st>>>((const float*)A, lda, nrows, ncols, diag_col, rowmax, diag);
+  else
+    k_rowmax_diag<double><<<nrows, 256, 0, st>>>((const double*)A, lda, nrows, ncols, diag_col, rowmax, diag);
+  return cudaGetLastError();
+}
+
+}  // namespace hvb

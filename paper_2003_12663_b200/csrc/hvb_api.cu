@@ -1,0 +1,205 @@
+// C-ABI of libhvb.so (declared in include/hvb.h).  Every entry point takes
+// raw device pointers owned by the caller (PyTorch tensors on the Python
+// side), sizes and a cudaStream_t, launches asynchronously and returns 0 or
+// an HVB_E* status; hvb_last_error() gives the message.  No torch types, no
+// allocation, no host synchronisation.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/hvb.h"
+#include "launch.cuh"
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* what, cudaError_t e = cudaSuccess) {
+  char buf[512];
+  if (e != cudaSuccess)
+    snprintf(buf, sizeof buf, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+  else
+    snprintf(buf, sizeof buf, "%s", what);
+  g_err = buf;
+  return code;
+}
+
+static int check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return fail(HVB_ECUDA, what, e);
+  return HVB_OK;
+}
+
+extern "C" {
+
+const char* hvb_last_error(void) { return g_err.c_str(); }
+
+int hvb_version(void) { return HVB_ABI_VERSION; }
+
+int hvb_build_table(const double* nodes6, int nt, int nq, const double* rule, double* table, void* stream) {
+  if (nt < 0 || (nq != 3 && nq != 6 && nq != 12 && nq != 16)) return fail(HVB_EARG, "hvb_build_table: bad nt/nq");
+  if (nt == 0) return HVB_OK;
+  return check(hvb::launch_build_table(nodes6, nt, nq, rule, table, (cudaStream_t)stream), "hvb_build_table");
+}
+
+int hvb_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
+                     const int* ent_meta, long long n_entries, double* stream_out, void* stream) {
+  if (n_entries < 0) return fail(HVB_EARG, "hvb_build_stream: negative entry count");
+  return check(hvb::launch_build_stream(table, nq, ccr, eta, ent_tri, ent_meta, n_entries, stream_out,
+                                        (cudaStream_t)stream),
+               "hvb_build_stream");
+}
+
+int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_col0,
+                         const int* tile_width, int n_tiles, int nq, int row_begin, int n_rows, const double* rowdata,
+                         const int* row_kind, const int* row_col, const double* row_scale,
+                         const long long* row_out, double* A, const int* tri_cols, int mode, int warps_per_block,
+                         int* near_list, unsigned long long* near_count, long long near_cap, void* stream) {
+  if (n_rows <= 0 || n_tiles <= 0) return HVB_OK;
+  if (mode < 0 || mode > 2 || warps_per_block < 1 || warps_per_block > 8)
+    return fail(HVB_EARG, "hvb_assemble_regular: bad mode / warps_per_block");
+  hvb::RegularArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.stream = panel_stream;
+  a.tile_ptr = (const int64_t*)tile_ptr;
+  a.tile_col0 = tile_col0;
+  a.tile_width = tile_width;
+  a.n_tiles = n_tiles;
+  a.row_begin = row_begin;
+  a.n_rows = n_rows;
+  a.rowdata = rowdata;
+  a.row_kind = row_kind;
+  a.row_col = row_col;
+  a.row_scale = row_scale;
+  a.row_out = (const int64_t*)row_out;
+  a.A = A;
+  a.tri_cols = tri_cols;
+  a.near_list = near_list;
+  a.near_count = near_count;
+  a.near_cap = near_cap;
+  return check(hvb::launch_regular(a, nq, mode, warps_per_block, (cudaStream_t)stream), "hvb_assemble_regular");
+}
+
+int hvb_assemble_singular(const double* nodes6, const int* tri_cols, const int* col_dev, const int* vc_ptr,
+                          const int* vc_tri, const int* vc_corner, const double* rule, int n_rule, int n_rows,
+                          const double* rowdata, const int* row_kind, const int* row_col, const double* row_scale,
+                          const double* row_diag, const long long* row_out, double* A, void* stream) {
+  hvb::SingularArgs a;
+  a.nodes6 = nodes6;
+  a.tri_cols = tri_cols;
+  a.col_dev = col_dev;
+  a.vc_ptr = vc_ptr;
+  a.vc_tri = vc_tri;
+  a.vc_corner = vc_corner;
+  a.rule = rule;
+  a.nm = n_rule;
+  a.rows = nullptr;
+  a.n_rows = n_rows;
+  a.rowdata = rowdata;
+  a.row_kind = row_kind;
+  a.row_col = row_col;
+  a.row_scale = row_scale;
+  a.row_diag = row_diag;
+  a.row_out = (const int64_t*)row_out;
+  a.A = A;
+  return check(hvb::launch_singular(a, (cudaStream_t)stream), "hvb_assemble_singular");
+}
+
+int hvb_fill_float_cols(double* A, const long long* row_out, const int* row_float, int n_rows, int n, int n_fl,
+                        void* stream) {
+  return check(hvb::launch_fill_float_cols(A, (const int64_t*)row_out, row_float, n_rows, n, n_fl,
+                                           (cudaStream_t)stream),
+               "hvb_fill_float_cols");
+}
+
+int hvb_near_pairs(const int* pairs, long long n_pairs, const double* points, const int* kind,
+                   const double* nodes6, const double* radii, const double* duffy, int n_duffy,
+                   const double* graded, int n_graded, int bisect_depth, double bisect_trigger, double* out,
+                   void* stream) {
+  hvb::NearArgs a;
+  a.pairs = pairs;
+  a.n_pairs = n_pairs;
+  a.points = points;
+  a.kind = kind;
+  a.nodes6 = nodes6;
+  a.radii = radii;
+  a.duffy = duffy;
+  a.n_duffy = n_duffy;
+  a.graded = graded;
+  a.n_graded = n_graded;
+  a.bisect_depth = bisect_depth;
+  a.bisect_trigger = bisect_trigger;
+  a.out = out;
+  return check(hvb::launch_near_pairs(a, (cudaStream_t)stream), "hvb_near_pairs");
+}
+
+int hvb_near_apply_rows(const int* seg_ptr, int n_seg, const int* pairs, const double* contrib,
+                        const int* tri_cols, const int* col_dev, const double* row_scale, const long long* row_out,
+                        double* A, void* stream) {
+  return check(hvb::launch_near_apply_rows(seg_ptr, n_seg, pairs, contrib, tri_cols, col_dev, row_scale,
+                                           (const int64_t*)row_out, A, (cudaStream_t)stream),
+               "hvb_near_apply_rows");
+}
+
+int hvb_gemv(const void* A, int is_f32, long long lda, int n_rows, int n_cols, const double* x, const double* left,
+             double* y, void* stream) {
+  if (lda < n_cols || (lda % 4) != 0) return fail(HVB_EARG, "hvb_gemv: lda must be >= n_cols and a multiple of 4");
+  return check(hvb::launch_gemv(A, is_f32, lda, n_rows, n_cols, x, left, y, (cudaStream_t)stream), "hvb_gemv");
+}
+
+int hvb_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp, void* stream) {
+  return check(hvb::launch_gather_scale(z, right, perm, n, xp, (cudaStream_t)stream), "hvb_gather_scale");
+}
+
+int hvb_rowmax_diag(const void* A, int is_f32, long long lda, int n_rows, int n_cols, const int* diag_col,
+                    double* rowmax, double* diag, void* stream) {
+  return check(hvb::launch_rowmax_diag(A, is_f32, lda, n_rows, n_cols, diag_col, rowmax, diag,
+                                       (cudaStream_t)stream),
+               "hvb_rowmax_diag");
+}
+
+int hvb_contract(const double* table, int nt, int nq, const int* tri_cols, const double* u, double* src,
+                 void* stream) {
+  return check(hvb::launch_contract(table, nt, nq, tri_cols, u, src, (cudaStream_t)stream), "hvb_contract");
+}
+
+int hvb_field(const double* src, const double* cls, const int* tri_cols, int nt, int nq, const double* pts,
+              const int* own_col, int m, int split, int potential, double* part, int* near_list,
+              unsigned long long* near_count, long long near_cap, void* stream) {
+  if (split < 1) return fail(HVB_EARG, "hvb_field: split must be >= 1");
+  hvb::FieldArgs a;
+  a.src = src;
+  a.cls = cls;
+  a.tri_cols = tri_cols;
+  a.nt = nt;
+  a.nq = nq;
+  a.pts = pts;
+  a.own_col = own_col;
+  a.m = m;
+  a.split = split;
+  a.potential = potential;
+  a.part = part;
+  a.near_list = near_list;
+  a.near_count = near_count;
+  a.near_cap = near_cap;
+  return check(hvb::launch_field(a, (cudaStream_t)stream), "hvb_field");
+}
+
+int hvb_field_reduce(const double* part, int split, int m, double* out, void* stream) {
+  return check(hvb::launch_field_reduce(part, split, m, out, (cudaStream_t)stream), "hvb_field_reduce");
+}
+
+int hvb_near_apply_points(const int* seg_ptr, int n_seg, const int* pairs, const double* contrib,
+                          const int* tri_cols, const double* u, int potential, double* out, void* stream) {
+  return check(hvb::launch_near_apply_points(seg_ptr, n_seg, pairs, contrib, tri_cols, u, potential, out,
+                                             (cudaStream_t)stream),
+               "hvb_near_apply_points");
+}
+
+int hvb_field_singular(const double* nodes6, const int* tri_cols, const int* vc_ptr, const int* vc_tri,
+                       const int* vc_corner, const double* rule, int n_rule, const double* pts,
+                       const double* normals, const int* own_col, int m, const double* u, double side,
+                       double* efield, double* emag, void* stream) {
+  return check(hvb::launch_field_singular(nodes6, tri_cols, vc_ptr, vc_tri, vc_corner, rule, n_rule, pts, normals,
+                                          own_col, m, u, side, efield, emag, (cudaStream_t)stream),
+               "hvb_field_singular");
+}
+
+}  // extern "C"

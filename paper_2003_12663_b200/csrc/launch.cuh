@@ -1,0 +1,111 @@
+// Argument blocks and launcher prototypes shared by the kernel files and
+// the C-ABI layer (hvb_api.cu).
+#pragma once
+#include "common.cuh"
+
+namespace hvb {
+
+struct RegularArgs {
+  const double* stream;     // tile panel streams, records of REC doubles
+  const int64_t* tile_ptr;  // (n_tiles+1) record offsets
+  const int* tile_col0;     // first device column of each tile
+  const int* tile_width;    // owned columns of each tile
+  int n_tiles;
+  int row_begin;            // first row-list entry of this launch
+  int n_rows;               // rows in this launch
+  const double* rowdata;    // RowData per row-list entry (6 doubles)
+  const int* row_kind;      // 0 SL, 1 ADL  (per row-list entry)
+  const int* row_col;       // own collocation column (singular test), -1 none
+  const double* row_scale;  // multiplies every entry of the row
+  const int64_t* row_out;   // output row offset (in elements) into A
+  double* A;                // output matrix (device column order)
+  const int* tri_cols;      // (nt,3) original collocation cols of corners
+  int* near_list;           // (cap, 2): (row-list index, triangle)
+  unsigned long long* near_count;
+  long long near_cap;
+};
+
+struct SingularArgs {
+  const double* nodes6;
+  const int* tri_cols;    // original cols
+  const int* col_dev;     // original col -> device col
+  const int* vc_ptr;      // star CSR over original collocation cols
+  const int* vc_tri;
+  const int* vc_corner;
+  const double* rule;     // 3 x nm x 4
+  int nm;
+  const int* rows;        // row-list entries to process
+  int n_rows;
+  const double* rowdata;
+  const int* row_kind;
+  const int* row_col;
+  const double* row_scale;
+  const double* row_diag;  // added to A[row, own col] after scaling
+  const int64_t* row_out;
+  double* A;
+};
+
+struct NearArgs {
+  const int* pairs;        // (np, 2): point index, triangle
+  long long n_pairs;
+  const double* points;    // (m, 6): x, y, z, nx, ny, nz
+  const int* kind;         // per point: 0 SL, 1 ADL, 2 E (vector), 3 potential
+  const double* nodes6;    // (nt, 18)
+  const double* radii;     // (nt)
+  const double* duffy;     // (n_duffy, 4) Duffy(0, near_duffy_points)
+  int n_duffy;
+  const double* graded;    // (n_graded, 4) graded(depth, n1d, outer)
+  int n_graded;
+  int bisect_depth;
+  double bisect_trigger;
+  double* out;             // (np, 9) corner contributions
+};
+
+struct FieldArgs {
+  const double* src;      // (nt, nq, 4) contracted sources
+  const double* cls;      // (nt, 6): cc, thr, thr2_lo, thr2_hi
+  const int* tri_cols;    // (nt, 3) original cols (singular test)
+  int nt, nq;
+  const double* pts;      // (m, 3) targets
+  const int* own_col;     // (m) own collocation col or -1 (may be null)
+  int m;
+  int split;              // panel-range split (grid.y)
+  int potential;          // 1: phi, 0: E
+  double* part;           // (split, m, 4) partial sums
+  int* near_list;         // (cap, 2): (target, triangle)
+  unsigned long long* near_count;
+  long long near_cap;
+};
+
+size_t regular_smem_bytes(int nq, int wpb);
+cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, int wpb, cudaStream_t st);
+cudaError_t launch_build_table(const double* nodes6, int nt, int nq, const double* rule, double* out,
+                               cudaStream_t st);
+cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
+                                const int* ent_meta, int64_t ne, double* out, cudaStream_t st);
+cudaError_t launch_singular(const SingularArgs& a, cudaStream_t st);
+cudaError_t launch_fill_float_cols(double* A, const int64_t* row_out, const int* row_float, int n_rows, int n,
+                                   int n_fl, cudaStream_t st);
+cudaError_t launch_near_pairs(const NearArgs& a, cudaStream_t st);
+cudaError_t launch_near_apply_rows(const int* seg_ptr, int n_seg, const int* pairs, const double* contrib,
+                                   const int* tri_cols, const int* col_dev, const double* row_scale,
+                                   const int64_t* row_out, double* A, cudaStream_t st);
+cudaError_t launch_gemv(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const double* x,
+                        const double* left, double* y, cudaStream_t st);
+cudaError_t launch_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp,
+                                cudaStream_t st);
+cudaError_t launch_rowmax_diag(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const int* diag_col,
+                               double* rowmax, double* diag, cudaStream_t st);
+cudaError_t launch_field(const FieldArgs& a, cudaStream_t st);
+cudaError_t launch_contract(const double* table, int nt, int nq, const int* tri_cols, const double* u, double* src,
+                            cudaStream_t st);
+cudaError_t launch_field_reduce(const double* part, int split, int m, double* out, cudaStream_t st);
+cudaError_t launch_near_apply_points(const int* seg_ptr, int n_seg, const int* pairs, const double* contrib,
+                                     const int* tri_cols, const double* u, int potential, double* out,
+                                     cudaStream_t st);
+cudaError_t launch_field_singular(const double* nodes6, const int* tri_cols, const int* vc_ptr, const int* vc_tri,
+                                  const int* vc_corner, const double* rule, int nm, const double* pts,
+                                  const double* normals, const int* own_col, int m, const double* u, double side,
+                                  double* efield, double* emag, cudaStream_t st);
+
+}  // namespace hvb

@@ -1,0 +1,228 @@
+"""Device-resident mesh data and the column-tile schedule of the regular sweep.
+
+Host side (NumPy, once per mesh):
+
+* ``column_tiling`` -- the matrix is stored in a *device column order*:
+  recursive coordinate bisection of the collocation points into compact
+  tiles of at most ``max_tile`` columns, each tile swept along its longest
+  axis.  A panel that touches a tile contributes to its *owned* corners
+  only; within a tile the owned corners of any panel lie within ``band``
+  columns of its first owned corner, which is what lets the assembly kernel
+  keep a 96-column sliding window per warp (csrc/assemble.cu).  Panels with
+  corners in several tiles are evaluated once per tile (``redundancy``).
+* entries (tile, panel) sorted by (tile, first owned column).
+
+Device side (``DeviceMesh``, cached per device/config): panel nodes,
+circumcircles, sample tables (K1), the packed panel streams, rule tables
+(regular, corner Duffy, near Duffy, graded composite), CSR stars.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .quadrature import QuadConfig, duffy_rule, graded_rule, regular_rule
+
+__all__ = ["ColumnTiling", "column_tiling", "DeviceMesh", "device_mesh", "WINDOW_BAND"]
+
+WINDOW_BAND = 64  # csrc/assemble.cu: WIN - 32
+
+
+@dataclass
+class ColumnTiling:
+    perm: np.ndarray        # device col -> original col (n,)
+    inv: np.ndarray         # original col -> device col (n,)
+    tile_col0: np.ndarray   # (n_tiles,)
+    tile_width: np.ndarray  # (n_tiles,)
+    tile_ptr: np.ndarray    # (n_tiles+1,) entry offsets
+    ent_tri: np.ndarray     # (ne,) panel of each entry
+    ent_meta: np.ndarray    # (ne, 5): mfirst, l0, l1, l2, flags
+    band: int
+    redundancy: float
+
+
+def _rcb(points: np.ndarray, idx: np.ndarray, max_tile: int, out: list):
+    """Recursive coordinate bisection (median split on the longest axis)."""
+    stack = [idx]
+    while stack:
+        cur = stack.pop()
+        if len(cur) <= max_tile:
+            out.append(cur)
+            continue
+        p = points[cur]
+        ax = int(np.argmax(p.max(axis=0) - p.min(axis=0)))
+        order = np.argsort(p[:, ax], kind="stable")
+        h = len(cur) // 2
+        # push the second half first so tiles come out in sweep order
+        stack.append(cur[order[h:]])
+        stack.append(cur[order[:h]])
+
+
+def _sweep(points: np.ndarray, tile: np.ndarray) -> np.ndarray:
+    p = points[tile]
+    ax = int(np.argmax(p.max(axis=0) - p.min(axis=0)))
+    return tile[np.argsort(p[:, ax], kind="stable")]
+
+
+def _entries(tri_cols: np.ndarray, tile_of: np.ndarray, local: np.ndarray):
+    nt = len(tri_cols)
+    ct = tile_of[tri_cols]  # (nt, 3) tile of each corner
+    cl = local[tri_cols]
+    tri = np.repeat(np.arange(nt), 3)
+    tl = ct.ravel()
+    # unique (panel, tile) pairs
+    key = tri.astype(np.int64) * (int(tile_of.max()) + 1) + tl
+    key = np.unique(key)
+    e_tri = key // (int(tile_of.max()) + 1)
+    e_tile = key % (int(tile_of.max()) + 1)
+    owned = ct[e_tri] == e_tile[:, None]  # (ne, 3)
+    loc = np.where(owned, cl[e_tri], -1)
+    big = np.iinfo(np.int64).max
+    mfirst = np.where(owned, loc, big).min(axis=1)
+    mlast = np.where(owned, loc, -1).max(axis=1)
+    primary = (ct[e_tri, 0] == e_tile).astype(np.int64)
+    return e_tri, e_tile, loc, mfirst, mlast, primary
+
+
+def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = 2048,
+                  band_max: int = WINDOW_BAND) -> ColumnTiling:
+    n = len(points)
+    tri_cols = np.asarray(tri_cols, dtype=np.int64)
+    tiles: list = []
+    _rcb(points, np.arange(n), max_tile, tiles)
+    for _ in range(40):
+        tiles = [_sweep(points, t) for t in tiles]
+        tile_of = np.empty(n, dtype=np.int64)
+        local = np.empty(n, dtype=np.int64)
+        for k, t in enumerate(tiles):
+            tile_of[t] = k
+            local[t] = np.arange(len(t))
+        e_tri, e_tile, loc, mfirst, mlast, primary = _entries(tri_cols, tile_of, local)
+        band_e = mlast - mfirst
+        per_tile = np.zeros(len(tiles), dtype=np.int64)
+        np.maximum.at(per_tile, e_tile, band_e)
+        bad = np.nonzero(per_tile > band_max)[0]
+        if len(bad) == 0:
+            break
+        bad_set = set(bad.tolist())
+        nxt: list = []
+        for k, t in enumerate(tiles):
+            if k in bad_set and len(t) > 1:
+                _rcb(points, t, max(1, len(t) // 2), nxt)
+            else:
+                nxt.append(t)
+        tiles = nxt
+    else:  # pragma: no cover - pathological mesh
+        raise RuntimeError("column tiling: could not bound the panel band")
+    perm = np.concatenate(tiles).astype(np.int64)
+    inv = np.empty(n, dtype=np.int64)
+    inv[perm] = np.arange(n)
+    widths = np.array([len(t) for t in tiles], dtype=np.int64)
+    col0 = np.concatenate([[0], np.cumsum(widths)[:-1]])
+    order = np.lexsort((e_tri, mfirst, e_tile))
+    e_tri, e_tile, loc, mfirst, primary = e_tri[order], e_tile[order], loc[order], mfirst[order], primary[order]
+    counts = np.bincount(e_tile, minlength=len(tiles))
+    tile_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    meta = np.column_stack([mfirst, loc, primary]).astype(np.int32)
+    return ColumnTiling(
+        perm=perm, inv=inv, tile_col0=col0.astype(np.int32), tile_width=widths.astype(np.int32),
+        tile_ptr=tile_ptr, ent_tri=e_tri.astype(np.int32), ent_meta=meta,
+        band=int(per_tile.max()) if len(per_tile) else 0,
+        redundancy=float(len(e_tri)) / max(1, len(tri_cols)),
+    )
+
+
+def _rule4(rule) -> np.ndarray:
+    out = np.zeros((len(rule), 4))
+    out[:, :2] = rule.nodes
+    out[:, 2] = rule.weights
+    return out
+
+
+class DeviceMesh:
+    """All per-mesh device buffers for one (device, quadrature config)."""
+
+    def __init__(self, mesh, cfg: QuadConfig, device, max_tile: int = 2048):
+        import torch
+
+        self.device = device
+        self.cfg = cfg
+        f64 = dict(dtype=torch.float64, device=device)
+        i32 = dict(dtype=torch.int32, device=device)
+        self.n = mesh.n_collocation
+        self.nt = mesh.n_triangles
+        self.nodes6 = torch.as_tensor(mesh.tri_nodes.reshape(self.nt, 18), **f64).contiguous()
+        self.tri_cols = torch.as_tensor(mesh.tri_corner_cols, **i32).contiguous()
+        ccr = np.column_stack([mesh.circumcenters, mesh.circumradii])
+        self.ccr = torch.as_tensor(ccr, **f64).contiguous()
+        self.radii = torch.as_tensor(mesh.circumradii, **f64)
+        self.points = torch.as_tensor(mesh.colloc_points, **f64).contiguous()
+        self.normals = torch.as_tensor(mesh.colloc_normals, **f64).contiguous()
+        self.vc_ptr = torch.as_tensor(mesh.vc_ptr, **i32)
+        self.vc_tri = torch.as_tensor(mesh.vc_tri, **i32)
+        self.vc_corner = torch.as_tensor(mesh.vc_corner, **i32)
+        # classification bracket per panel (field kernels): cc, thr, lo, hi
+        thr = cfg.eta * mesh.circumradii
+        cls = np.column_stack([mesh.circumcenters, thr, thr * thr * (1 - 1e-13), thr * thr * (1 + 1e-13)])
+        self.cls = torch.as_tensor(cls, **f64).contiguous()
+
+        # rule tables
+        reg = regular_rule(cfg.regular_order)
+        self.nq = len(reg)
+        self.rule_regular = torch.as_tensor(_rule4(reg), **f64)
+        self.rule_duffy = torch.as_tensor(
+            np.concatenate([_rule4(duffy_rule(c, cfg.duffy_points)) for c in range(3)]), **f64)
+        self.n_duffy = len(duffy_rule(0, cfg.duffy_points))
+        self.rule_near = torch.as_tensor(_rule4(duffy_rule(0, cfg.near_duffy_points)), **f64)
+        self.rule_graded = torch.as_tensor(
+            _rule4(graded_rule(cfg.bisect_depth, cfg.near_duffy_points, cfg.near_outer_order)), **f64)
+
+        st = _lib.stream_ptr(device)
+        # K1 sample table
+        self.table = torch.empty((self.nt, self.nq, 6), **f64)
+        _lib.call("hvb_build_table", _lib.ptr(self.nodes6), self.nt, self.nq, _lib.ptr(self.rule_regular),
+                  _lib.ptr(self.table), st)
+
+        # column tiling + panel streams
+        tiling = mesh_tiling(mesh, max_tile)
+        self.tiling = tiling
+        self.perm = torch.as_tensor(tiling.perm, **i32)
+        self.col_dev = torch.as_tensor(tiling.inv, **i32)
+        self.tile_ptr = torch.as_tensor(tiling.tile_ptr, dtype=torch.int64, device=device)
+        self.tile_col0 = torch.as_tensor(tiling.tile_col0, **i32)
+        self.tile_width = torch.as_tensor(tiling.tile_width, **i32)
+        ent_tri = torch.as_tensor(tiling.ent_tri, **i32)
+        ent_meta = torch.as_tensor(tiling.ent_meta, **i32).contiguous()
+        ne = len(tiling.ent_tri)
+        self.rec = 6 * self.nq + 8
+        self.stream = torch.empty((ne, self.rec), **f64)
+        _lib.call("hvb_build_stream", _lib.ptr(self.table), self.nq, _lib.ptr(self.ccr), float(cfg.eta),
+                  _lib.ptr(ent_tri), _lib.ptr(ent_meta), ne, _lib.ptr(self.stream), st)
+        self.n_tiles = len(tiling.tile_width)
+
+
+def mesh_tiling(mesh, max_tile: int = 2048) -> ColumnTiling:
+    key = ("tiling", max_tile)
+    cache = mesh._device_cache
+    t = cache.get(key)
+    if t is None:
+        t = column_tiling(mesh.colloc_points, mesh.tri_corner_cols, max_tile=max_tile)
+        cache[key] = t
+    return t
+
+
+def device_mesh(mesh, cfg: QuadConfig | None = None, device=None) -> DeviceMesh:
+    cfg = cfg or QuadConfig()
+    dev = _lib.require_device(device)
+    key = ("dm", str(dev), cfg)
+    dm = mesh._device_cache.get(key)
+    if dm is None:
+        import torch
+
+        with torch.cuda.device(dev):
+            dm = DeviceMesh(mesh, cfg, dev)
+        mesh._device_cache[key] = dm
+    return dm
