@@ -108,12 +108,13 @@ def partition_rows(total: int, n_blocks: int) -> list:
 class DeviceStore:
     """Row-major (rows, lda) device matrix in device column order."""
 
-    def __init__(self, tensor, n: int, size: int, perm_t, perm_np):
+    def __init__(self, tensor, n: int, size: int, perm_t, perm_np, row0: int = 0):
         self.A = tensor          # torch (rows, lda)
         self.n = n
         self.size = size
         self.perm_t = perm_t     # torch int32 (n,) device col -> original col, or None
         self.perm = perm_np      # numpy (n,) or None (identity)
+        self.row0 = row0         # global index of the first stored row
 
     @property
     def lda(self) -> int:
@@ -225,13 +226,12 @@ def _rowmax_diag(st: DeviceStore):
 
     dev = st.A.device
     rows = st.A.shape[0]
-    diag_col = torch.arange(rows, dtype=torch.int32, device=dev)
+    g = np.arange(st.row0, st.row0 + rows)  # global row -> its diagonal column
     if st.perm is not None:
         inv = np.empty(st.n, dtype=np.int64)
         inv[st.perm] = np.arange(st.n)
-        dc = np.arange(rows)
-        dc[: st.n] = inv[: min(rows, st.n)] if rows >= st.n else inv[:rows]
-        diag_col = torch.as_tensor(dc, dtype=torch.int32, device=dev)
+        g = np.where(g < st.n, inv[np.minimum(g, st.n - 1)], g)
+    diag_col = torch.as_tensor(g, dtype=torch.int32, device=dev)
     rowmax = torch.empty(rows, dtype=torch.float64, device=dev)
     diag = torch.empty(rows, dtype=torch.float64, device=dev)
     _lib.call("hvb_rowmax_diag", _lib.ptr(st.A), int(st.is_f32), st.lda, rows, st.size,
@@ -312,6 +312,28 @@ def _plan(dev, x, nrm, kind, col, scale, diag, out_off) -> RowPlan:
     )
 
 
+LAST_NEAR_ROWS = None  # near pairs per collocation row of the last assembly (bench roofline)
+
+# Optional phase profiler (bench.py): a list that receives
+# (label, start_event, end_event) triples recorded on the launching stream.
+PROFILE = None
+
+
+def _mark():
+    if PROFILE is None:
+        return None
+    import torch
+
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def _span(label, e0):
+    if PROFILE is not None and e0 is not None:
+        PROFILE.append((label, e0, _mark()))
+
+
 def _run_rows(dm, plan: RowPlan, A, counts: dict, warps_per_block: int = 4):
     """Regular + near + singular passes for one row plan writing into A."""
     import torch
@@ -321,6 +343,7 @@ def _run_rows(dm, plan: RowPlan, A, counts: dict, warps_per_block: int = 4):
     if plan.m == 0:
         return
     cap = max(4096, 16 * plan.m)
+    e_reg = _mark()
     while True:
         near = torch.empty((cap, 2), dtype=torch.int32, device=dev)
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -336,7 +359,12 @@ def _run_rows(dm, plan: RowPlan, A, counts: dict, warps_per_block: int = 4):
         if n_near <= cap:
             break
         cap = n_near + 1024  # overflow: rerun with room (regular entries are simply rewritten)
+    _span("regular", e_reg)
     counts["near"] += n_near
+    if n_near:
+        per = torch.bincount(near[:n_near, 0].long(), minlength=plan.m).cpu().numpy()
+        counts.setdefault("near_rows", []).append((plan.col.cpu().numpy(), per))
+    e_near = _mark()
     if n_near:
         pairs = _sort_pairs(near[:n_near], dm.nt)
         contrib = torch.empty((n_near, 9), dtype=torch.float64, device=dev)
@@ -348,10 +376,13 @@ def _run_rows(dm, plan: RowPlan, A, counts: dict, warps_per_block: int = 4):
         _lib.call("hvb_near_apply_rows", _lib.ptr(seg), len(seg) - 1, _lib.ptr(pairs), _lib.ptr(contrib),
                   _lib.ptr(dm.tri_cols), _lib.ptr(dm.col_dev), _lib.ptr(plan.scale), _lib.ptr(plan.out),
                   _lib.ptr(A), s)
+    _span("near", e_near)
+    e_sing = _mark()
     _lib.call("hvb_assemble_singular", _lib.ptr(dm.nodes6), _lib.ptr(dm.tri_cols), _lib.ptr(dm.col_dev),
               _lib.ptr(dm.vc_ptr), _lib.ptr(dm.vc_tri), _lib.ptr(dm.vc_corner), _lib.ptr(dm.rule_duffy),
               dm.n_duffy, plan.m, _lib.ptr(plan.rowdata), _lib.ptr(plan.kind), _lib.ptr(plan.col),
               _lib.ptr(plan.scale), _lib.ptr(plan.diag), _lib.ptr(plan.out), _lib.ptr(A), s)
+    _span("singular", e_sing)
 
 
 def _sort_pairs(pairs, nt: int):
@@ -445,27 +476,7 @@ def assemble(mesh: SurfaceMesh, cfg: QuadConfig | None = None, n_blocks: int = 1
             raise AssemblyError(f"floating surface {k} has zero area")
     ranges = partition_rows(size, n_blocks)
     dm = _device_mesh(mesh, cfg, device)
-    dev = dm.device
-    lda = -(-size // LDA_ALIGN) * LDA_ALIGN
-    with torch.cuda.device(dev):
-        A = torch.empty((size, lda), dtype=torch.float64, device=dev)
-        rows = np.arange(n)
-        kind, scale, diag = _row_coeffs(mesh, rows)
-        plan = _plan(dev, mesh.colloc_points, mesh.colloc_normals, kind, rows, scale, diag, rows * lda)
-        counts = {"near": 0}
-        _run_rows(dm, plan, A, counts)
-        if mesh.n_floating:
-            rf = torch.as_tensor(mesh.row_float.astype(np.int32), device=dev)
-            ro = torch.as_tensor((rows * lda).astype(np.int64), device=dev)
-            _lib.call("hvb_fill_float_cols", _lib.ptr(A), _lib.ptr(ro), _lib.ptr(rf), n, n, mesh.n_floating,
-                      _lib.stream_ptr(dev))
-            for k in range(mesh.n_floating):
-                adl, ids = _neutrality_scales(mesh, k)
-                row = A[n + k]
-                row[n:size] = 0.0
-                row[:n] = _weighted_adl_sum(mesh, dm, mesh.floating_collocation(k), adl, ids)
-        if precision == "single":
-            A = A.to(torch.float32)
+    A, counts = assemble_rows(mesh, dm, 0, size, precision)
     store = DeviceStore(A, n, size, dm.perm, dm.tiling.perm)
     blocks = [RowBlock(a, b, store=store) for a, b in ranges]
     rhs = np.where(mesh.row_kind_code == 0, mesh.row_v0, 0.0)
@@ -485,6 +496,46 @@ def assemble(mesh: SurfaceMesh, cfg: QuadConfig | None = None, n_blocks: int = 1
         "tile_redundancy": dm.tiling.redundancy,
     }
     return matrix, rhs
+
+
+def assemble_rows(mesh: SurfaceMesh, dm, start: int, stop: int, precision: str = "double"):
+    """Device rows [start, stop) of the system (a row block of
+    ``partition_rows``) as a (stop-start, lda) tensor in device column
+    order, plus pair counts over its collocation rows.  Every row is computed
+    independently of the block boundaries, so any partition gives bitwise
+    identical rows (reference invariance, tests/test_assembly.py:146-158)."""
+    import torch
+
+    n = mesh.n_collocation
+    size = n + mesh.n_floating
+    dev = dm.device
+    lda = -(-size // LDA_ALIGN) * LDA_ALIGN
+    counts = {"near": 0}
+    with torch.cuda.device(dev):
+        A = torch.empty((stop - start, lda), dtype=torch.float64, device=dev)
+        rows = np.arange(start, min(stop, n))
+        if len(rows):
+            kind, scale, diag = _row_coeffs(mesh, rows)
+            off = (rows - start) * lda
+            plan = _plan(dev, mesh.colloc_points[rows], mesh.colloc_normals[rows], kind, rows, scale, diag, off)
+            _run_rows(dm, plan, A, counts)
+            global LAST_NEAR_ROWS
+            LAST_NEAR_ROWS = np.zeros(n, dtype=np.int64)
+            for cols, per in counts.get("near_rows", []):
+                LAST_NEAR_ROWS[cols] += per
+            if mesh.n_floating:
+                rf = torch.as_tensor(mesh.row_float[rows].astype(np.int32), device=dev)
+                ro = torch.as_tensor(off.astype(np.int64), device=dev)
+                _lib.call("hvb_fill_float_cols", _lib.ptr(A), _lib.ptr(ro), _lib.ptr(rf), len(rows), n,
+                          mesh.n_floating, _lib.stream_ptr(dev))
+        for k in range(max(start, n), stop):
+            adl, ids = _neutrality_scales(mesh, k - n)
+            row = A[k - start]
+            row[n:size] = 0.0
+            row[:n] = _weighted_adl_sum(mesh, dm, mesh.floating_collocation(k - n), adl, ids)
+        if precision == "single":
+            A = A.to(torch.float32)
+    return A, counts
 
 
 def _device_mesh(mesh, cfg, device):
