@@ -126,6 +126,8 @@ int hvb_field_singular(const double* nodes6, const int* tri_cols, const int* vc_
 /* Roofline denominators measured on the box (bench.py): DFMA throughput
  * kernel (blocks x 256 threads x iters x 64 FMAs) and a read-only stream. */
 int hvb_bench_dfma(double* out, int blocks, int iters, void* stream);
+int hvb_bench_latency(double* out, int n, void* stream);
+int hvb_bench_nodes(double* out, int var, int blocks, int threads, int iters, void* stream);
 int hvb_bench_read(const double* p, long long n, double* out, int blocks, void* stream);
 
 #ifdef __cplusplus

@@ -38,6 +38,8 @@ SIGNATURES = {
     "hvb_near_apply_points": [_P, _I, _P, _P, _P, _P, _I, _P, _P],
     "hvb_field_singular": [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P, _D, _P, _P, _P],
     "hvb_bench_dfma": [_P, _I, _I, _P],
+    "hvb_bench_latency": [_P, _I, _P],
+    "hvb_bench_nodes": [_P, _I, _I, _I, _I, _P],
     "hvb_bench_read": [_P, _LL, _P, _I, _P],
 }
 

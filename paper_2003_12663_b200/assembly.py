@@ -334,6 +334,11 @@ def _span(label, e0):
         PROFILE.append((label, e0, _mark()))
 
 
+# warps per CTA of the regular sweep (csrc/assemble_dual.cu; ~29 KB of
+# shared memory per warp -> 7 resident warps per SM with 1-warp CTAs)
+_WPB = int(__import__("os").environ.get("HVB_ASM_WPB", "1"))
+
+
 def _run_rows(dm, plan: RowPlan, A, counts: dict, warps_per_block: int = 4):
     """Regular + near + singular passes for one row plan writing into A."""
     import torch
@@ -353,7 +358,8 @@ def _run_rows(dm, plan: RowPlan, A, counts: dict, warps_per_block: int = 4):
                     "hvb_assemble_regular", _lib.ptr(dm.stream), _lib.ptr(dm.tile_ptr), _lib.ptr(dm.tile_col0),
                     _lib.ptr(dm.tile_width), dm.n_tiles, dm.nq, lo, hi - lo, _lib.ptr(plan.rowdata),
                     _lib.ptr(plan.kind), _lib.ptr(plan.col), _lib.ptr(plan.scale), _lib.ptr(plan.out),
-                    _lib.ptr(A), _lib.ptr(dm.tri_cols), mode, warps_per_block, _lib.ptr(near), _lib.ptr(cnt),
+                    _lib.ptr(A), _lib.ptr(dm.tri_cols), mode | (4 if dm.window == 64 else 0), _WPB,
+                    _lib.ptr(near), _lib.ptr(cnt),
                     cap, s)
         n_near = int(cnt.item())
         if n_near <= cap:

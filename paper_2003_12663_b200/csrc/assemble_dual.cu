@@ -1,0 +1,284 @@
+// Production regular sweep (K2+K3): "dual" layout.
+//
+// A warp owns 32 rows and a sliding window of WIN owned columns in shared
+// memory (win[slot][row], padded row stride).  Each step consumes a PAIR of
+// consecutive panel records of the column tile: lanes 0-15 evaluate record
+// 2p, lanes 16-31 record 2p+1, and every lane evaluates its record for TWO
+// rows (lane&15 and lane&15 + 16).  So each node's data (one 48-byte
+// broadcast load) feeds two independent FP64 chains, the per-record control
+// work is shared by two rows, and every row has two panels in flight.
+//
+// Record format (6*NQ+8 doubles, built by hvb_build_stream): NQ nodes x
+// (y, jw*hat_0..2/4pi), circumcentre, thr=fl(eta R), squared bracket,
+// int tri, int mfirst, short slot[3] (= owned local column % WIN, or WIN
+// for a corner owned by another tile -> a dump slot), short flags.
+//
+// Window adds go stream 0 then stream 1, so every matrix entry is summed in
+// a fixed order (bitwise reproducible, independent of the row blocking).
+// The host tiling guarantees both records of a pair fit the window
+// (pair band <= WIN - 32).  Classification is the reference's exact
+// decision (common.cuh); non-regular non-singular pairs are emitted once
+// (primary tile) for the deferred near-singular pass.
+//
+// Kernel values: SL uses the MUFU seed + one Newton step (rel. error
+// ~1e-12, entries are sums of positive terms); ADL keeps the cubic step
+// (signed sums, cancellation).
+#include "launch.cuh"
+
+namespace hvb {
+namespace dual {
+constexpr int ROWS = 32;
+constexpr int STRIDE = 33;
+constexpr int RING = 3;
+template <int WIN>
+struct Shape {
+  static constexpr int SLOTS = WIN + 1;                    // + dump slot
+  static constexpr int WREG = (SLOTS * STRIDE + 1) & ~1;   // 16-byte aligned region
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+}  // namespace dual
+
+template <int NQ, int MODE, int WIN>
+__global__ void __launch_bounds__(64) k_assemble_dual(RegularArgs a) {
+  using namespace dual;
+  constexpr int REC = 6 * NQ + 8;
+  constexpr int PREC = 2 * REC;
+  constexpr int SLOTS = Shape<WIN>::SLOTS;
+  constexpr int WREG = Shape<WIN>::WREG;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int rl = lane & 15;
+  const int sidx = lane >> 4;
+  const int wib = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  double* win = smem + wib * (WREG + RING * PREC);
+  double* ring = win + WREG;
+
+  const int rowtile = blockIdx.x * wpb + wib;
+  const int tile = blockIdx.y;
+  if (rowtile * ROWS >= a.n_rows) return;
+  const int base_row = rowtile * ROWS;
+
+  // the two compute rows of this lane
+  const int i0 = base_row + rl, i1 = base_row + rl + 16;
+  const bool live0 = i0 < a.n_rows, live1 = i1 < a.n_rows;
+  const int lr0 = a.row_begin + (live0 ? i0 : a.n_rows - 1);
+  const int lr1 = a.row_begin + (live1 ? i1 : a.n_rows - 1);
+  const double* rd0 = a.rowdata + 6 * (size_t)lr0;
+  const double* rd1 = a.rowdata + 6 * (size_t)lr1;
+  const d3 X0 = mk3(rd0[0], rd0[1], rd0[2]);
+  const d3 X1 = mk3(rd1[0], rd1[1], rd1[2]);
+  const d3 N0 = mk3(rd0[3], rd0[4], rd0[5]);
+  const d3 N1 = mk3(rd1[3], rd1[4], rd1[5]);
+  const bool adl0 = (MODE == 1) || (MODE == 2 && a.row_kind[lr0] == 1);
+  const bool adl1 = (MODE == 1) || (MODE == 2 && a.row_kind[lr1] == 1);
+  const int own0 = a.row_col[lr0], own1 = a.row_col[lr1];
+  // the flush row of this lane (row base_row + lane)
+  const int fi = base_row + lane;
+  const bool flive = fi < a.n_rows;
+  const int flr = a.row_begin + (flive ? fi : a.n_rows - 1);
+  const int64_t fout = flive ? a.row_out[flr] : -1;
+  const double fscale = a.row_scale[flr];
+
+  for (int k = lane; k < SLOTS * STRIDE; k += 32) win[k] = 0.0;
+
+  const int64_t e0 = a.tile_ptr[tile], e1 = a.tile_ptr[tile + 1];
+  const int col0 = a.tile_col0[tile], width = a.tile_width[tile];
+  const double* src = a.stream + e0 * REC;
+  const int64_t ne = e1 - e0;
+  const int64_t np = (ne + 1) >> 1;
+
+  auto stage = [&](int64_t p) {
+    double* dst = ring + (p % RING) * PREC;
+    const double* s = src + 2 * p * REC;
+    const int nch = (2 * p + 1 < ne) ? REC : REC / 2;
+    for (int c = lane; c < nch; c += 32) dual::cp_async16(dst + 2 * c, s + 2 * c);
+  };
+#pragma unroll
+  for (int s = 0; s < RING - 1; ++s) {
+    if (s < np) stage(s);
+    dual::commit();
+  }
+
+  int base = 0;
+  auto flush32 = [&](int b) {
+    const int c = b + lane;
+    double* wcol = win + (c % WIN) * STRIDE;
+    const bool in = c < width;
+#pragma unroll 8
+    for (int j = 0; j < ROWS; ++j) {
+      const int64_t off = __shfl_sync(0xffffffffu, fout, j);
+      const double sc = __shfl_sync(0xffffffffu, fscale, j);
+      if (off >= 0 && in) a.A[off + col0 + c] = wcol[j] * sc;
+      wcol[j] = 0.0;
+    }
+    __syncwarp();
+  };
+
+  for (int64_t p = 0; p < np; ++p) {
+    dual::wait_group<RING - 2>();
+    __syncwarp();
+    const double* pr = ring + (p % RING) * PREC;
+    {
+      const int64_t nxt = p + RING - 1;
+      if (nxt < np) stage(nxt);
+      dual::commit();
+    }
+    const int mfirst0 = reinterpret_cast<const int*>(pr + 6 * NQ + 6)[1];
+    while (mfirst0 >= base + 32) {
+      flush32(base);
+      base += 32;
+    }
+    const bool valid = 2 * p + sidx < ne;
+    const double* rec = pr + sidx * REC;
+    const double* cg = rec + 6 * NQ;
+    const d3 C = mk3(cg[0], cg[1], cg[2]);
+    const double sq0 = sumsq_unfused(sub_rn(X0, C));
+    const double sq1 = sumsq_unfused(sub_rn(X1, C));
+
+    double a00 = 0.0, a01 = 0.0, a02 = 0.0, a10 = 0.0, a11 = 0.0, a12 = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const double2 p01 = *reinterpret_cast<const double2*>(rec + 6 * q);
+      const double2 p2w = *reinterpret_cast<const double2*>(rec + 6 * q + 2);
+      const double2 w12 = *reinterpret_cast<const double2*>(rec + 6 * q + 4);
+      const double dx0 = X0.x - p01.x, dy0 = X0.y - p01.y, dz0 = X0.z - p2w.x;
+      const double dx1 = X1.x - p01.x, dy1 = X1.y - p01.y, dz1 = X1.z - p2w.x;
+      const double r20 = fma(dz0, dz0, fma(dy0, dy0, dx0 * dx0));
+      const double r21 = fma(dz1, dz1, fma(dy1, dy1, dx1 * dx1));
+      double k0, k1;
+      if (MODE == 0) {
+        k0 = rsqrt_newton(r20);
+        k1 = rsqrt_newton(r21);
+      } else {
+        const double ri0 = rsqrt_full(r20);
+        const double ri1 = rsqrt_full(r21);
+        const double dn0 = fma(dz0, N0.z, fma(dy0, N0.y, dx0 * N0.x));
+        const double dn1 = fma(dz1, N1.z, fma(dy1, N1.y, dx1 * N1.x));
+        const double ka0 = dn0 * (ri0 * ri0 * ri0);
+        const double ka1 = dn1 * (ri1 * ri1 * ri1);
+        k0 = (MODE == 1) ? ka0 : (adl0 ? ka0 : ri0);
+        k1 = (MODE == 1) ? ka1 : (adl1 ? ka1 : ri1);
+      }
+      a00 = fma(k0, p2w.y, a00);
+      a01 = fma(k0, w12.x, a01);
+      a02 = fma(k0, w12.y, a02);
+      a10 = fma(k1, p2w.y, a10);
+      a11 = fma(k1, w12.x, a11);
+      a12 = fma(k1, w12.y, a12);
+    }
+    bool reg0 = sq0 > cg[5];
+    if (!reg0 && !(sq0 < cg[4])) reg0 = __dsqrt_rn(sq0) > cg[3];
+    bool reg1 = sq1 > cg[5];
+    if (!reg1 && !(sq1 < cg[4])) reg1 = __dsqrt_rn(sq1) > cg[3];
+    if (!reg0) a00 = a01 = a02 = 0.0;
+    if (!reg1) a10 = a11 = a12 = 0.0;
+
+    const int* meta = reinterpret_cast<const int*>(cg + 6);
+    const unsigned sl01 = static_cast<unsigned>(meta[2]);
+    const unsigned sl2f = static_cast<unsigned>(meta[3]);
+    const int s0 = valid ? (int)(sl01 & 0xffffu) : WIN;
+    const int s1 = valid ? (int)(sl01 >> 16) : WIN;
+    const int s2 = valid ? (int)(sl2f & 0xffffu) : WIN;
+    const bool primary = valid && (sl2f >> 16) & 1u;
+
+    // deferred near pairs (rare): emitted from the panel's primary tile only
+    const bool nr0 = !reg0 && primary && live0;
+    const bool nr1 = !reg1 && primary && live1;
+    if (__any_sync(0xffffffffu, nr0 || nr1)) {
+      const int tri = meta[0];
+      const int* tc = a.tri_cols + 3 * (size_t)tri;
+      const bool em0 = nr0 && !(tc[0] == own0 || tc[1] == own0 || tc[2] == own0);
+      const bool em1 = nr1 && !(tc[0] == own1 || tc[1] == own1 || tc[2] == own1);
+      const unsigned m0 = __ballot_sync(0xffffffffu, em0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, em1);
+      unsigned long long b = 0;
+      if (lane == 0 && (m0 | m1)) b = atomicAdd(a.near_count, (unsigned long long)(__popc(m0) + __popc(m1)));
+      b = __shfl_sync(0xffffffffu, b, 0);
+      const unsigned lt = (1u << lane) - 1u;
+      if (em0) {
+        const long long slot = (long long)b + __popc(m0 & lt);
+        if (slot < a.near_cap) {
+          a.near_list[2 * slot] = a.row_begin + i0;
+          a.near_list[2 * slot + 1] = tri;
+        }
+      }
+      if (em1) {
+        const long long slot = (long long)b + __popc(m0) + __popc(m1 & lt);
+        if (slot < a.near_cap) {
+          a.near_list[2 * slot] = a.row_begin + i1;
+          a.near_list[2 * slot + 1] = tri;
+        }
+      }
+    }
+
+    // window adds: stream 0 (record 2p) then stream 1 (record 2p+1)
+    double* w0 = win + s0 * STRIDE + rl;
+    double* w1 = win + s1 * STRIDE + rl;
+    double* w2 = win + s2 * STRIDE + rl;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (sidx == s) {
+        w0[0] += a00;
+        w0[16] += a10;
+        w1[0] += a01;
+        w1[16] += a11;
+        w2[0] += a02;
+        w2[16] += a12;
+      }
+      __syncwarp();
+    }
+  }
+  dual::wait_group<0>();
+  __syncwarp();
+  while (base < width) {
+    flush32(base);
+    base += 32;
+  }
+}
+
+template <int WIN>
+static size_t dual_smem_bytes(int nq, int wpb) {
+  return (size_t)wpb * (dual::Shape<WIN>::WREG + dual::RING * 2 * (6 * nq + 8)) * sizeof(double);
+}
+
+template <int NQ, int WIN>
+static cudaError_t launch_dual_nq(const RegularArgs& a, int mode, int wpb, cudaStream_t st) {
+  dim3 grid((a.n_rows + dual::ROWS * wpb - 1) / (dual::ROWS * wpb), a.n_tiles);
+  const size_t smem = dual_smem_bytes<WIN>(NQ, wpb);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 32 * wpb, smem, st>>>(a);
+    return cudaGetLastError();
+  };
+  if (mode == 0) return go(k_assemble_dual<NQ, 0, WIN>);
+  if (mode == 1) return go(k_assemble_dual<NQ, 1, WIN>);
+  return go(k_assemble_dual<NQ, 2, WIN>);
+}
+
+template <int WIN>
+static cudaError_t launch_dual(const RegularArgs& a, int nq, int mode, int wpb, cudaStream_t st) {
+  switch (nq) {
+    case 3: return launch_dual_nq<3, WIN>(a, mode, wpb, st);
+    case 6: return launch_dual_nq<6, WIN>(a, mode, wpb, st);
+    case 12: return launch_dual_nq<12, WIN>(a, mode, wpb, st);
+    case 16: return launch_dual_nq<16, WIN>(a, mode, wpb, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// window: 96 (pair band <= 64) or 64 (pair band <= 32)
+cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, int window, int wpb, cudaStream_t st) {
+  if (window == 64) return launch_dual<64>(a, nq, mode, wpb, st);
+  if (window == 96) return launch_dual<96>(a, nq, mode, wpb, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hvb

@@ -50,6 +50,17 @@ HVB_DEV double rsqrt_full(double r2) {
   return __fma_rn(u, t, y);
 }
 
+// MUFU.RSQ64H seed + one Newton step (4 FP64 ops, relative error ~1e-12):
+// used for the single-layer kernel, whose regular entries are sums of
+// positive terms (entry error <= node error, 100x inside the 1e-10 parity).
+HVB_DEV double rsqrt_newton(double r2) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+  const double h = r2 * y;
+  const double e = __fma_rn(-h, y, 1.0);
+  return __fma_rn(y * 0.5, e, y);
+}
+
 // Classification "regular iff ||x - cc|| > eta R" exactly as the reference
 // decides it (sqrt of the unfused sum, strict compare against fl(eta*R)).
 // thr = fl(eta*R) and the squared bracket [lo, hi] are precomputed per

@@ -53,7 +53,9 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
                          const long long* row_out, double* A, const int* tri_cols, int mode, int warps_per_block,
                          int* near_list, unsigned long long* near_count, long long near_cap, void* stream) {
   if (n_rows <= 0 || n_tiles <= 0) return HVB_OK;
-  if (mode < 0 || mode > 2 || warps_per_block < 1 || warps_per_block > 8)
+  const int window = (mode & 4) ? 64 : 96;  // bit 2: 64-column window tiling
+  mode &= 3;
+  if (mode > 2 || warps_per_block < 1 || warps_per_block > 8)
     return fail(HVB_EARG, "hvb_assemble_regular: bad mode / warps_per_block");
   hvb::RegularArgs a;
   std::memset(&a, 0, sizeof a);
@@ -74,7 +76,8 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
   a.near_list = near_list;
   a.near_count = near_count;
   a.near_cap = near_cap;
-  return check(hvb::launch_regular(a, nq, mode, warps_per_block, (cudaStream_t)stream), "hvb_assemble_regular");
+  return check(hvb::launch_regular(a, nq, mode, window, warps_per_block, (cudaStream_t)stream),
+               "hvb_assemble_regular");
 }
 
 int hvb_assemble_singular(const double* nodes6, const int* tri_cols, const int* col_dev, const int* vc_ptr,

@@ -77,8 +77,7 @@ struct FieldArgs {
   long long near_cap;
 };
 
-size_t regular_smem_bytes(int nq, int wpb);
-cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, int wpb, cudaStream_t st);
+cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, int window, int wpb, cudaStream_t st);
 cudaError_t launch_build_table(const double* nodes6, int nt, int nq, const double* rule, double* out,
                                cudaStream_t st);
 cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,

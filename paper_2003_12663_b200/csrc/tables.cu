@@ -1,0 +1,160 @@
+// Assembly support kernels: regular-rule sample table (K1), panel-stream
+// packing, the singular Duffy pass (K4) and the floating columns (K6).  The
+// regular sweep itself is csrc/assemble_dual.cu.
+//
+// Reference: TriangleTables src/assembly.py:73-118, row_pass1 singular batch
+// 202-235, _row_equation 408-468.
+#include "launch.cuh"
+
+namespace hvb {
+
+// K1: regular-rule sample table.  out[t][q] = (y_tq, jw_tq*hat_c(q)/(4 pi))
+// (reference TriangleTables.__init__, src/assembly.py:78-103).
+__global__ void k_build_table(const double* __restrict__ nodes6, int nt, int nq,
+                              const double* __restrict__ rule,  // nq x 4: u, v, w, pad
+                              double* __restrict__ out) {
+  int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= nt * nq) return;
+  int t = gid / nq, q = gid % nq;
+  double u = rule[4 * q], v = rule[4 * q + 1], w = rule[4 * q + 2];
+  d3 p;
+  double jac;
+  curved_point(nodes6 + 18 * (size_t)t, u, v, p, jac);
+  double jw = w * jac * kInv4Pi;
+  double* o = out + 6 * (size_t)gid;
+  o[0] = p.x; o[1] = p.y; o[2] = p.z;
+  o[3] = jw * (1.0 - u - v);
+  o[4] = jw * u;
+  o[5] = jw * v;
+}
+
+// Pack one stream record per (tile, panel) entry.
+__global__ void k_build_stream(const double* __restrict__ table, int nq,
+                               const double* __restrict__ ccr,  // (nt,4): cc, R
+                               double eta, const int* __restrict__ ent_tri,
+                               const int* __restrict__ ent_meta,  // (ne,5): mfirst, slot0, slot1, slot2, flags
+                               int64_t ne, double* __restrict__ out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  const int rec = 6 * nq + 8;
+  int t = ent_tri[e];
+  double* o = out + e * rec;
+  const double* s = table + (size_t)t * 6 * nq;
+  for (int k = 0; k < 6 * nq; ++k) o[k] = s[k];
+  const double* c = ccr + 4 * (size_t)t;
+  double thr = __dmul_rn(eta, c[3]);
+  double t2 = thr * thr;
+  o[6 * nq + 0] = c[0];
+  o[6 * nq + 1] = c[1];
+  o[6 * nq + 2] = c[2];
+  o[6 * nq + 3] = thr;
+  o[6 * nq + 4] = t2 * (1.0 - 1e-13);
+  o[6 * nq + 5] = t2 * (1.0 + 1e-13);
+  int* m = reinterpret_cast<int*>(o + 6 * nq + 6);
+  const int* em = ent_meta + 5 * e;
+  m[0] = t;
+  m[1] = em[0];
+  short* l = reinterpret_cast<short*>(m + 2);
+  for (int c = 0; c < 3; ++c) l[c] = (short)em[1 + c];  // window slots, computed on the host
+  l[3] = (short)em[4];
+}
+
+// K4: singular (corner) pairs.  One warp per row; the row's star panels are
+// processed in triangle order (reference row_pass1 singular batch,
+// src/assembly.py:202-235) and added to the row after the regular sweep.
+// Duffy rule tables per corner: rule[c][m] = (u, v, w, pad).
+
+
+__global__ void k_assemble_singular(SingularArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= a.n_rows) return;
+  const double* rd = a.rowdata + 6 * (size_t)w;
+  const d3 X = mk3(rd[0], rd[1], rd[2]);
+  const double nx = rd[3], ny = rd[4], nz = rd[5];
+  const bool adl = a.row_kind[w] == 1;
+  const int own = a.row_col[w];
+  const double sc = a.row_scale[w];
+  double* Arow = a.A + a.row_out[w];
+  if (own < 0) return;
+  for (int s = a.vc_ptr[own]; s < a.vc_ptr[own + 1]; ++s) {
+    const int t = a.vc_tri[s], c = a.vc_corner[s];
+    const double* Xn = a.nodes6 + 18 * (size_t)t;
+    const double* R = a.rule + (size_t)c * a.nm * 4;
+    double s0 = 0, s1 = 0, s2 = 0;
+    for (int m = lane; m < a.nm; m += 32) {
+      double u = R[4 * m], v = R[4 * m + 1], wq = R[4 * m + 2];
+      d3 p;
+      double jac;
+      curved_point(Xn, u, v, p, jac);
+      double dx = X.x - p.x, dy = X.y - p.y, dz = X.z - p.z;
+      double r = sqrt(dx * dx + dy * dy + dz * dz);
+      double k = adl ? (dx * nx + dy * ny + dz * nz) / (r * r * r) : 1.0 / r;
+      k *= wq * jac * kInv4Pi;
+      s0 = fma(k, 1.0 - u - v, s0);
+      s1 = fma(k, u, s1);
+      s2 = fma(k, v, s2);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      const int* tc = a.tri_cols + 3 * (size_t)t;
+      Arow[a.col_dev[tc[0]]] += sc * s0;
+      Arow[a.col_dev[tc[1]]] += sc * s1;
+      Arow[a.col_dev[tc[2]]] += sc * s2;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) Arow[a.col_dev[own]] += a.row_diag[w];
+}
+
+// Columns n .. N-1 (floating potentials) of collocation rows: -1 in the
+// row's own floating column, 0 elsewhere (reference src/assembly.py:425-426).
+__global__ void k_fill_float_cols(double* A, const int64_t* row_out, const int* row_float, int n_rows,
+                                  int n, int n_fl) {
+  int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= (int64_t)n_rows * n_fl) return;
+  int r = (int)(g / n_fl), k = (int)(g % n_fl);
+  A[row_out[r] + n + k] = (row_float[r] == k) ? -1.0 : 0.0;
+}
+
+}  // namespace hvb
+
+// ---------------------------------------------------------------------------
+// launchers (called by hvb_api.cu)
+// ---------------------------------------------------------------------------
+namespace hvb {
+
+cudaError_t launch_build_table(const double* nodes6, int nt, int nq, const double* rule, double* out,
+                               cudaStream_t st) {
+  int n = nt * nq;
+  k_build_table<<<(n + 255) / 256, 256, 0, st>>>(nodes6, nt, nq, rule, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, double eta,
+                                const int* ent_tri, const int* ent_meta, int64_t ne, double* out,
+                                cudaStream_t st) {
+  if (ne == 0) return cudaSuccess;
+  k_build_stream<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(table, nq, ccr, eta, ent_tri, ent_meta, ne, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_singular(const SingularArgs& a, cudaStream_t st) {
+  if (a.n_rows == 0) return cudaSuccess;
+  int threads = 128;
+  int blocks = (a.n_rows * 32 + threads - 1) / threads;
+  k_assemble_singular<<<blocks, threads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_float_cols(double* A, const int64_t* row_out, const int* row_float, int n_rows,
+                                   int n, int n_fl, cudaStream_t st) {
+  int64_t tot = (int64_t)n_rows * n_fl;
+  if (tot == 0) return cudaSuccess;
+  k_fill_float_cols<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A, row_out, row_float, n_rows, n, n_fl);
+  return cudaGetLastError();
+}
+
+}  // namespace hvb

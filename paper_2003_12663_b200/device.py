@@ -28,7 +28,12 @@ from .quadrature import QuadConfig, duffy_rule, graded_rule, regular_rule
 
 __all__ = ["ColumnTiling", "column_tiling", "DeviceMesh", "device_mesh", "WINDOW_BAND"]
 
-WINDOW_BAND = 64  # csrc/assemble.cu: WIN - 32
+WINDOW_BAND = 64  # csrc/assemble_dual.cu: WIN - 32 for the default 96-column window
+# regular-sweep window (96 or 64 columns) and tile shape; env overrides are
+# for A/B measurements (tools/ab.sh)
+WINDOW = int(__import__("os").environ.get("HVB_ASM_WIN", "64"))
+STRIPS = __import__("os").environ.get("HVB_ASM_STRIPS", "1") == "1"
+MAX_TILE = int(__import__("os").environ.get("HVB_ASM_MAXTILE", "32767"))
 
 
 @dataclass
@@ -87,8 +92,25 @@ def _entries(tri_cols: np.ndarray, tile_of: np.ndarray, local: np.ndarray):
     return e_tri, e_tile, loc, mfirst, mlast, primary
 
 
+def _split_across(points: np.ndarray, tile: np.ndarray):
+    """Halve a tile across its sweep direction (median split on the
+    second-longest axis): the sweep front halves, the tile stays a strip."""
+    p = points[tile]
+    ext = p.max(axis=0) - p.min(axis=0)
+    ax = int(np.argsort(ext)[-2])
+    order = np.argsort(p[:, ax], kind="stable")
+    h = len(tile) // 2
+    return [tile[order[:h]], tile[order[h:]]]
+
+
 def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = 2048,
-                  band_max: int = WINDOW_BAND) -> ColumnTiling:
+                  band_max: int = WINDOW_BAND, group: int = 2, strips: bool = False) -> ColumnTiling:
+    """Column tiles + sorted (tile, panel) entries.  The band is measured
+    over groups of ``group`` consecutive records of each tile (starting at
+    the tile's first record), as the grouped assembly kernel keeps a whole
+    group in its window at once.  ``strips``: tiles of up to ``max_tile``
+    columns that violate the band are split ACROSS their sweep axis (long
+    strips, fewer boundary panels) instead of recursively bisected."""
     n = len(points)
     tri_cols = np.asarray(tri_cols, dtype=np.int64)
     tiles: list = []
@@ -101,7 +123,20 @@ def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = 2048
             tile_of[t] = k
             local[t] = np.arange(len(t))
         e_tri, e_tile, loc, mfirst, mlast, primary = _entries(tri_cols, tile_of, local)
+        order = np.lexsort((e_tri, mfirst, e_tile))
+        e_tri, e_tile, loc, mfirst, mlast, primary = (x[order] for x in (e_tri, e_tile, loc, mfirst, mlast,
+                                                                          primary))
+        counts = np.bincount(e_tile, minlength=len(tiles))
+        tile_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
         band_e = mlast - mfirst
+        if group > 1 and len(e_tri):
+            pos = np.arange(len(e_tri)) - tile_ptr[e_tile]
+            gid = e_tile * (int(counts.max()) + group) + pos // group  # group key
+            first = np.nonzero(pos % group == 0)[0]
+            gmax = np.full(len(e_tri), -1, dtype=np.int64)
+            np.maximum.at(gmax, np.searchsorted(gid[first], gid), mlast)
+            band_e = np.zeros_like(band_e)
+            band_e[first] = gmax[: len(first)] - mfirst[first]
         per_tile = np.zeros(len(tiles), dtype=np.int64)
         np.maximum.at(per_tile, e_tile, band_e)
         bad = np.nonzero(per_tile > band_max)[0]
@@ -111,7 +146,10 @@ def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = 2048
         nxt: list = []
         for k, t in enumerate(tiles):
             if k in bad_set and len(t) > 1:
-                _rcb(points, t, max(1, len(t) // 2), nxt)
+                if strips:
+                    nxt.extend(_split_across(points, t))
+                else:
+                    _rcb(points, t, max(1, len(t) // 2), nxt)
             else:
                 nxt.append(t)
         tiles = nxt
@@ -122,10 +160,6 @@ def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = 2048
     inv[perm] = np.arange(n)
     widths = np.array([len(t) for t in tiles], dtype=np.int64)
     col0 = np.concatenate([[0], np.cumsum(widths)[:-1]])
-    order = np.lexsort((e_tri, mfirst, e_tile))
-    e_tri, e_tile, loc, mfirst, primary = e_tri[order], e_tile[order], loc[order], mfirst[order], primary[order]
-    counts = np.bincount(e_tile, minlength=len(tiles))
-    tile_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
     meta = np.column_stack([mfirst, loc, primary]).astype(np.int32)
     return ColumnTiling(
         perm=perm, inv=inv, tile_col0=col0.astype(np.int32), tile_width=widths.astype(np.int32),
@@ -145,7 +179,7 @@ def _rule4(rule) -> np.ndarray:
 class DeviceMesh:
     """All per-mesh device buffers for one (device, quadrature config)."""
 
-    def __init__(self, mesh, cfg: QuadConfig, device, max_tile: int = 2048):
+    def __init__(self, mesh, cfg: QuadConfig, device, max_tile: int = MAX_TILE):
         import torch
 
         self.device = device
@@ -187,7 +221,8 @@ class DeviceMesh:
                   _lib.ptr(self.table), st)
 
         # column tiling + panel streams
-        tiling = mesh_tiling(mesh, max_tile)
+        self.window = WINDOW
+        tiling = mesh_tiling(mesh, max_tile, WINDOW, STRIPS)
         self.tiling = tiling
         self.perm = torch.as_tensor(tiling.perm, **i32)
         self.col_dev = torch.as_tensor(tiling.inv, **i32)
@@ -195,7 +230,10 @@ class DeviceMesh:
         self.tile_col0 = torch.as_tensor(tiling.tile_col0, **i32)
         self.tile_width = torch.as_tensor(tiling.tile_width, **i32)
         ent_tri = torch.as_tensor(tiling.ent_tri, **i32)
-        ent_meta = torch.as_tensor(tiling.ent_meta, **i32).contiguous()
+        meta = tiling.ent_meta.copy()
+        loc = meta[:, 1:4]
+        meta[:, 1:4] = np.where(loc >= 0, loc % WINDOW, WINDOW)  # window slots (WINDOW = dump slot)
+        ent_meta = torch.as_tensor(meta, **i32).contiguous()
         ne = len(tiling.ent_tri)
         self.rec = 6 * self.nq + 8
         self.stream = torch.empty((ne, self.rec), **f64)
@@ -204,12 +242,14 @@ class DeviceMesh:
         self.n_tiles = len(tiling.tile_width)
 
 
-def mesh_tiling(mesh, max_tile: int = 2048) -> ColumnTiling:
-    key = ("tiling", max_tile)
+def mesh_tiling(mesh, max_tile: int = 2048, window: int = 96, strips: bool = False) -> ColumnTiling:
+    """Host column tiling of a mesh (a mesh-derived array, cached on it)."""
+    key = ("tiling", max_tile, window, strips)
     cache = mesh._device_cache
     t = cache.get(key)
     if t is None:
-        t = column_tiling(mesh.colloc_points, mesh.tri_corner_cols, max_tile=max_tile)
+        t = column_tiling(mesh.colloc_points, mesh.tri_corner_cols, max_tile=max_tile, band_max=window - 32,
+                          strips=strips)
         cache[key] = t
     return t
 
