@@ -119,8 +119,9 @@ def _check_points(mesh: SurfaceMesh, X: np.ndarray):
     if tree is None:
         tree = cKDTree(mesh.vertices)
         mesh._device_cache["kdtree"] = tree
-    dist, idx = tree.query(X, k=1)
-    bad = np.nonzero(dist < 2 * VERTEX_PROXIMITY)[0]
+    # bounded search: only candidates within 1e-9 matter (far queries are free)
+    dist, idx = tree.query(X, k=1, distance_upper_bound=1e-9)
+    bad = np.nonzero(np.isfinite(dist))[0]
     for i in bad:
         d = _fp.norm3_axis(mesh.vertices - X[i][None, :])
         if d.min() < VERTEX_PROXIMITY:

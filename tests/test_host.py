@@ -1,0 +1,371 @@
+"""CPU tests of the host layer: C-ABI library, config, row partition,
+column tiling invariants, quadrature rules and decisions, mesh validation,
+streamer / ionization / CSV (reference semantics, tests/test_*.py)."""
+
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2003_12663_b200 import config, fixtures, quadrature
+from paper_2003_12663_b200.mesh import EPS0, MeshError, parse_mesh
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# ---------------------------------------------------------------------------
+# C ABI
+# ---------------------------------------------------------------------------
+
+
+def _header_functions():
+    text = open(os.path.join(ROOT, "include", "hvb.h")).read()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(hvb_\w+)\(", text, flags=re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    import ctypes
+
+    import __graft_entry__
+
+    __graft_entry__.build()
+    lib = ctypes.CDLL(__graft_entry__.LIB)
+    names = _header_functions()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(lib, name), name
+    lib.hvb_version.restype = ctypes.c_int
+    assert lib.hvb_version() == 1
+
+
+def test_binding_signatures_cover_header():
+    from paper_2003_12663_b200 import _lib
+
+    declared = set(_header_functions()) - {"hvb_last_error", "hvb_version"}
+    assert declared == set(_lib.SIGNATURES)
+
+
+def test_device_entry_points_fail_loudly_without_gpu():
+    import torch
+
+    from paper_2003_12663_b200 import _lib
+    from paper_2003_12663_b200.assembly import assemble
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(_lib.DeviceUnavailable):
+        assemble(fixtures.sphere_mesh(1))
+
+
+# ---------------------------------------------------------------------------
+# config / partition
+# ---------------------------------------------------------------------------
+
+
+def test_config_defaults_and_overrides(tmp_path):
+    c = config.Config()
+    assert c["quad.eta"] == 1.2 and c["solver.restart"] == 100
+    p = tmp_path / "run.cfg"
+    p.write_text("# comment\nquad.eta = 1.5\nsolver.row_equilibrate = off\n")
+    c = config.Config.load(p, overrides=["solver.rel_tol=1e-10"])
+    assert c["quad.eta"] == 1.5 and c["solver.row_equilibrate"] is False and c["solver.rel_tol"] == 1e-10
+    assert c.quad().eta == 1.5
+    assert c.solver().rel_tol == 1e-10
+    assert c.trace_params().rel_tol == 1e-6
+    with pytest.raises(KeyError):
+        config.Config({"quad.nope": 1})
+    with pytest.raises(ValueError):
+        c.set("solver.verbose", "maybe")
+
+
+def test_partition_rows_reference_semantics():
+    from paper_2003_12663_b200.assembly import partition_rows
+
+    assert partition_rows(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    assert partition_rows(10, 1) == [(0, 10)]
+    assert partition_rows(5, 5) == [(i, i + 1) for i in range(5)]
+    with pytest.raises(ValueError):
+        partition_rows(4, 5)
+
+
+def test_solver_config_validation():
+    from paper_2003_12663_b200.solver import SolverConfig
+
+    with pytest.raises(ValueError):
+        SolverConfig(restart=0)
+    with pytest.raises(ValueError):
+        SolverConfig(rel_tol=2.0)
+
+
+# ---------------------------------------------------------------------------
+# column tiling (device column order) invariants
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("maker,window,strips", [
+    (lambda: fixtures.sphere_mesh(3), 64, True),
+    (lambda: fixtures.close_gap_mesh(2), 96, False),
+    (lambda: fixtures.rod_plane_mesh(0.15), 64, True),
+])
+def test_column_tiling_invariants(maker, window, strips):
+    from paper_2003_12663_b200.device import column_tiling
+
+    m = maker()
+    T = column_tiling(m.colloc_points, m.tri_corner_cols, max_tile=4096, band_max=window - 32, strips=strips)
+    n = m.n_collocation
+    assert sorted(T.perm.tolist()) == list(range(n))
+    assert np.array_equal(T.inv[T.perm], np.arange(n))
+    assert T.tile_width.sum() == n and np.all(np.diff(T.tile_col0) == T.tile_width[:-1])
+    # every (panel, corner) is owned by exactly one entry; one primary entry per panel
+    owned = np.zeros((m.n_triangles, 3), dtype=int)
+    prim = np.zeros(m.n_triangles, dtype=int)
+    for k in range(len(T.tile_width)):
+        a, b = T.tile_ptr[k], T.tile_ptr[k + 1]
+        meta = T.ent_meta[a:b]
+        tri = T.ent_tri[a:b]
+        assert np.all(np.diff(meta[:, 0]) >= 0)  # sorted by first owned column
+        for e in range(b - a):
+            t = tri[e]
+            for c in range(3):
+                l = meta[e, 1 + c]
+                if l >= 0:
+                    owned[t, c] += 1
+                    # the owned local column is the corner's device column
+                    assert T.inv[m.tri_corner_cols[t, c]] == T.tile_col0[k] + l
+        prim[tri] += meta[:, 4]
+        # pair band fits the window
+        for e in range(0, b - a, 2):
+            grp = meta[e:e + 2, 1:4]
+            assert grp[grp >= 0].max() - meta[e, 0] <= window - 32
+    assert np.all(owned == 1)
+    assert np.all(prim == 1)
+
+
+# ---------------------------------------------------------------------------
+# quadrature (reference tests/test_quadrature.py semantics)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("order", [2, 4, 6, 8])
+def test_rules_exact(order):
+    r = quadrature.regular_rule(order)
+    assert abs(r.weights.sum() - 0.5) < 5e-15
+    u, v = r.nodes[:, 0], r.nodes[:, 1]
+    for i in range(order + 1):
+        for j in range(order + 1 - i):
+            exact = math.factorial(i) * math.factorial(j) / math.factorial(i + j + 2)
+            assert abs(np.sum(r.weights * u ** i * v ** j) - exact) < 5e-15
+    assert np.all(u >= 0) and np.all(v >= 0) and np.all(u + v <= 1)
+
+
+def test_unsupported_order():
+    with pytest.raises(quadrature.QuadratureError):
+        quadrature.regular_rule(5)
+    with pytest.raises(quadrature.QuadratureError):
+        quadrature.duffy_rule(0, 1)
+    with pytest.raises(quadrature.QuadratureError):
+        quadrature.duffy_rule(3, 6)
+
+
+def test_duffy_corner_singular_reference_value():
+    # CORNER_SINGULAR_REF of the reference tests: int 1/|y| over the unit
+    # right triangle from corner 0 = sqrt(2) asinh(1)
+    r = quadrature.duffy_rule(0, 8)
+    got = float(np.sum(r.weights / np.hypot(r.nodes[:, 0], r.nodes[:, 1])))
+    assert abs(got - math.sqrt(2.0) * math.asinh(1.0)) < 1e-8
+    assert abs(r.weights.sum() - 0.5) < 1e-14
+
+
+def test_rules_match_reference_golden(golden):
+    for c in range(3):
+        r = quadrature.duffy_rule(c, 6)
+        np.testing.assert_array_equal(r.nodes, golden[f"duffy{c}_nodes"])
+        np.testing.assert_array_equal(r.weights, golden[f"duffy{c}_weights"])
+    g = quadrature.graded_rule(3, 8, 8)
+    np.testing.assert_array_equal(g.nodes, golden["graded_nodes"])
+    np.testing.assert_array_equal(g.weights, golden["graded_weights"])
+
+
+def test_closest_point_decisions_match_reference(golden):
+    for row in golden["closest_cases"]:
+        cs = row[:9].reshape(3, 3)
+        assert quadrature.closest_point_flat(row[9:12], cs) == (row[12], row[13])
+
+
+NEAR_REFS = {0.1: 2.006576943826, 0.3: 1.437278726277, 0.6: 0.959761111114, 1.0: 0.645094888525}
+
+
+def test_near_singular_rule_accuracy_and_reference_nodes(golden):
+    corners = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0], [0.0, 1.0, 0.0]])
+    from paper_2003_12663_b200.mesh import _flat_circumcircle
+
+    c, R = _flat_circumcircle(corners)
+
+    class Tri:
+        nodes = np.vstack([corners, 0.5 * (corners[0] + corners[1]), 0.5 * (corners[1] + corners[2]),
+                           0.5 * (corners[2] + corners[0])])
+        circumradius = R
+
+    for frac, ref in NEAR_REFS.items():
+        x = corners.mean(axis=0) + np.array([0.0, 0.0, frac * R])
+        rule = quadrature.near_singular_rule(x, Tri)
+        pts = corners[0] + np.outer(rule.nodes[:, 0], corners[1]) + np.outer(rule.nodes[:, 1], corners[2])
+        got = float(np.sum(rule.weights / np.linalg.norm(pts - x, axis=1)))
+        assert abs(got - ref) / ref <= 1e-5
+        np.testing.assert_allclose(rule.nodes, golden[f"near_{frac}_nodes"], atol=1e-15, rtol=0)
+
+
+def test_subdivide_partitions_area():
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        u, v = rng.uniform(0, 1, 2)
+        if u + v > 1:
+            u, v = 1 - u, 1 - v
+        subs = quadrature.subdivide_at((u, v))
+        area = sum(0.5 * abs((s.corners[1][0] - s.corners[0][0]) * (s.corners[2][1] - s.corners[0][1])
+                             - (s.corners[1][1] - s.corners[0][1]) * (s.corners[2][0] - s.corners[0][0]))
+                   for s in subs)
+        assert abs(area - 0.5) < 1e-12
+    assert len(quadrature.subdivide_at((0.0, 0.0))) == 1
+    assert len(quadrature.subdivide_at((0.5, 0.0))) == 2
+    assert len(quadrature.subdivide_at((0.2, 0.3))) == 3
+
+
+def test_classify_pair_conformance():
+    rng = np.random.default_rng(123)
+    from paper_2003_12663_b200.mesh import CurvedTriangle, flat_circumcircles
+
+    for _ in range(2000):
+        cs = rng.uniform(-1, 1, (3, 3))
+        cc, r = flat_circumcircles(cs[None])
+        tri = CurvedTriangle(0, (0, 1, 2), (3, 4, 5), 0, np.vstack([cs, cs]), cc[0], float(r[0]))
+        if rng.uniform() < 0.3:
+            vid = int(rng.integers(0, 3))
+            assert quadrature.classify_pair(cs[vid], vid, tri).is_singular
+        else:
+            p = rng.uniform(-2, 2, 3)
+            want = "regular" if np.linalg.norm(p - cc[0]) > 1.2 * r[0] else "near_singular"
+            got = quadrature.classify_pair(p, 999, tri).kind
+            d = np.linalg.norm(p - cc[0])
+            if abs(d - 1.2 * r[0]) > 1e-12:
+                assert got == want
+
+
+# ---------------------------------------------------------------------------
+# mesh parsing / validation (reference tests/test_mesh.py messages)
+# ---------------------------------------------------------------------------
+
+FLAT = ("bemesh 1\nvertex 0 0 0 0\nvertex 1 1 0 0\nvertex 2 0 1 0\nvertex 3 0.5 0 0\n"
+        "vertex 4 0.5 0.5 0\nvertex 5 0 0.5 0\ntriangle 0 1 2 3 4 5 0\npatch 0 electrode 1.0\n")
+
+
+def test_parse_smallest_mesh():
+    m = parse_mesh(FLAT)
+    assert m.n_collocation == 3 and m.n_triangles == 1
+    assert abs(m.total_area() - 0.5) < 1e-14
+
+
+@pytest.mark.parametrize("text,frag", [
+    (FLAT.replace("triangle 0 1 2 3 4 5 0", "triangle 0 1 2 3 4 999 0"), "references vertex 999"),
+    ("vertex 0 0 0 0\n", "bemesh 1"),
+    (FLAT.replace("patch 0 electrode 1.0", "patch 7 electrode 1.0"), "unknown patch tag 0"),
+    (FLAT.replace("vertex 2 0 1 0", "vertex 2 2 0 0"), "degenerate triangle"),
+    (FLAT + "vertex 6 3 3 3\n", "belongs to no triangle"),
+    (FLAT.replace("patch 0 electrode 1.0", "patch 0 bogus 1.0"), "unknown patch kind"),
+])
+def test_parse_errors(text, frag):
+    with pytest.raises(MeshError, match=frag):
+        parse_mesh(text)
+
+
+def test_triple_junction_rejected():
+    v, tris = fixtures.sphere_mesh_parts(1)
+    ids = np.array([t[0] for t in tris])
+    tags = np.array([0 if k < len(tris) // 2 else 1 for k in range(len(tris))])
+    with pytest.raises(MeshError, match="triple junctions"):
+        fixtures.mesh_from_parts(v, ids, tags, ["patch 0 dielectric 1.0 2.0", "patch 1 dielectric 1.0 3.0"])
+
+
+def test_priority_electrode_over_dielectric():
+    v, tris = fixtures.sphere_mesh_parts(1)
+    ids = np.array([t[0] for t in tris])
+    tags = np.array([0 if k < len(tris) // 2 else 1 for k in range(len(tris))])
+    m = fixtures.mesh_from_parts(v, ids, tags, ["patch 0 electrode 2.0", "patch 1 dielectric 1.0 3.0"])
+    from paper_2003_12663_b200.mesh import Dirichlet, DielectricJump
+
+    kinds = m.row_kinds
+    assert any(isinstance(k, Dirichlet) for k in kinds) and any(isinstance(k, DielectricJump) for k in kinds)
+
+
+def test_relative_permittivity_and_roundtrip(tmp_path):
+    from paper_2003_12663_b200.mesh import load_mesh, save_mesh
+
+    m = parse_mesh(FLAT.replace("patch 0 electrode 1.0", "permittivity relative\npatch 0 dielectric 2.0 1.0"))
+    assert m.patches[0].eps_plus == 2.0 * EPS0
+    p = tmp_path / "m.bemesh"
+    save_mesh(fixtures.sphere_mesh(1), p)
+    again = load_mesh(p)
+    np.testing.assert_array_equal(again.vertices, fixtures.sphere_mesh(1).vertices)
+
+
+def test_lumped_weights_partition_area():
+    m = fixtures.sphere_mesh(2)
+    assert abs(m.total_area() - 4 * math.pi) / (4 * math.pi) < 5e-3
+    assert np.all(m.lumped_weights > 0)
+    assert np.allclose(np.linalg.norm(m.colloc_normals, axis=1), 1.0)
+
+
+def test_rod_plane_generator_config4():
+    m = fixtures.rod_plane_mesh(1.0)
+    assert 1.9e5 <= m.n_triangles <= 2.1e5
+    assert m.n_floating == 0
+    kinds = np.bincount(m.row_kind_code, minlength=3)
+    assert kinds[0] > 0 and kinds[2] > 0 and kinds[1] == 0
+
+
+# ---------------------------------------------------------------------------
+# streamer / ionization / field lines / CSV
+# ---------------------------------------------------------------------------
+
+
+def _straight(length=2.0, n=5, e=7.0):
+    from paper_2003_12663_b200.postprocess import FieldLine
+
+    s = np.linspace(0, length, n)
+    return FieldLine(np.column_stack([s, 0 * s, 0 * s]), np.full(n, e), s, "MaxLength")
+
+
+def test_streamer_integral():
+    from paper_2003_12663_b200.postprocess import IonizationModel, streamer_integral
+
+    line = _straight()
+    v, inc = streamer_integral(line, IonizationModel(np.array([0.0, 100.0]), np.array([5.0, 5.0]), 9.99))
+    assert abs(v - 10.0) < 1e-12 and inc
+    _, inc = streamer_integral(line, IonizationModel(np.array([0.0, 100.0]), np.array([5.0, 5.0]), 10.01))
+    assert not inc
+    with pytest.raises(ValueError):
+        IonizationModel(np.array([1.0, 1.0]), np.array([0.0, 1.0]), 1.0)
+
+
+def test_fieldline_validation_and_csv(tmp_path):
+    from paper_2003_12663_b200.postprocess import FieldLine, IonizationModel, load_ionization_model, write_fieldline_csv
+
+    with pytest.raises(ValueError):
+        FieldLine(np.zeros((2, 3)), np.zeros(2), np.zeros(2), "MaxLength")
+    p = tmp_path / "gas.txt"
+    p.write_text("# gas\n0.0 0.0\n2e6 10.0\nkstr 9.15\n")
+    model = load_ionization_model(p)
+    assert model.k_str == 9.15 and model.alpha(1e6) == pytest.approx(5.0) and model.alpha(4e6) == 10.0
+    q = tmp_path / "line.csv"
+    write_fieldline_csv(_straight(), IonizationModel(np.array([0.0, 100.0]), np.array([5.0, 5.0]), 1.0), q)
+    rows = q.read_text().strip().splitlines()
+    assert rows[0] == "x,y,z,s,E,alpha,cumulative_integral" and float(rows[-1].split(",")[6]) == pytest.approx(10.0)
+
+
+def test_demo_gas_file_shipped():
+    from paper_2003_12663_b200.postprocess import load_ionization_model
+
+    m = load_ionization_model(os.path.join(ROOT, "paper_2003_12663_b200", "data", "air_demo.gas"))
+    assert m.k_str == 9.15 and len(m.e_values) == 9
