@@ -123,6 +123,46 @@ int hvb_field_singular(const double* nodes6, const int* tri_cols, const int* vc_
                        const double* normals, const int* own_col, int m, const double* u, double side,
                        double* efield, double* emag, void* stream);
 
+/* K12-K14 -- device-resident field-line tracer (csrc/trace.cu).
+ * state: n_lines opaque records of hvb_line_state_bytes() bytes.
+ * geo: HOST pointer to 13 doubles = bbox centre (3), half extent x bbox_factor (3), diag,
+ * h_min, h_max, l_max, rel_tol, surface_tol_frac, e_floor.
+ * mode 0 initialises every line from starts/orient and requests E at the
+ * start; mode 1 consumes E results (e_out/e_flag, indexed by the previous
+ * request slots); mode 2 consumes surface distances (sd_out).  New E / SD
+ * requests are appended to e_pts/e_line and sd_pts/sd_line through
+ * counters[0] / counters[1]; counters[2] = max points per line; polylines (n_lines, cap, 5) = x, y, z, |E|, s.
+ * Replaces: trace_fieldline  postprocess.py:244-357 (control flow, step
+ * control, surface-hit snapping, termination order) */
+int hvb_line_state_bytes(void);
+int hvb_trace_ctrl(void* state, int n_lines, const double* starts, const int* orient, const double* geo, int mode,
+                   double* e_pts, int* e_line, double* sd_pts, int* sd_line, unsigned long long* counters,
+                   const double* e_out, const int* e_flag, const double* sd_out, double* out_pts,
+                   int cap, void* stream);
+
+/* per line (npts, termination, status, phase) and the start |E| of a
+ * weak-start line */
+int hvb_trace_summary(const void* state, int n_lines, int* info, double* dinfo, void* stream);
+
+/* K12 -- approximate distance to the curved surface and local circumradius
+ * at m points: 12 circumcircle candidates ranked by ||x-cc||-R, flat
+ * closest point mapped through the quadratic patch, first minimum wins.
+ * out (m, 2).  Replaces: _surface_distance  postprocess.py:198-218 */
+int hvb_surface_distance(const double* pts, int m, const double* ccr, int nt, const double* nodes6, double* out,
+                         void* stream);
+
+/* flag[i] = 1 for near-pair targets within prox of a node of the pair's
+ * panel.  Replaces: _check_point  postprocess.py:104-109 for tracer
+ * requests */
+int hvb_near_coincide(const int* pairs, long long n_pairs, const double* pts, const double* nodes6, double prox,
+                      int* flag, void* stream);
+
+/* K14 -- streamer integral per traced line: trapezoid of alpha(|E|)
+ * (linear table interpolation, constant outside) over arc length, verdict
+ * value > k_str.  Replaces: streamer_integral  postprocess.py:365-374 */
+int hvb_streamer(const double* out_pts, const void* state, int n_lines, int cap, const double* e_tab,
+                 const double* a_tab, int n_tab, double k_str, double* value, int* verdict, void* stream);
+
 /* Roofline denominators measured on the box (bench.py): DFMA throughput
  * kernel (blocks x 256 threads x iters x 64 FMAs) and a read-only stream. */
 int hvb_bench_dfma(double* out, int blocks, int iters, void* stream);

@@ -512,3 +512,111 @@ def streamer(arcs, mags, e_tab, a_tab, k_str):
     a = np.interp(mags, e_tab, a_tab)
     v = float(np.sum(0.5 * (a[1:] + a[:-1]) * np.diff(arcs)))
     return v, v > k_str
+
+
+# ---------------------------------------------------------------------------
+# surface distance and field-line tracer (postprocess.py:198-357)
+# ---------------------------------------------------------------------------
+
+
+def surface_distance(mesh, x, candidates=12):
+    """(d_surf, local R): 12 circumcircle candidates by ||x-cc||-R, flat
+    closest point mapped through the quadratic patch (postprocess.py:198-218)."""
+    x = np.asarray(x, dtype=float)
+    lower = axis_norm(mesh.circumcenters - x[None, :]) - mesh.circumradii
+    order = np.argsort(lower, kind="stable")[:candidates]
+    best, local = np.inf, mesh.circumradii[order[0]]
+    for t in order:
+        X6 = mesh.tri_nodes[t]
+        u, v = closest_point_flat(x, X6[0], X6[1], X6[2])
+        p, _ = curved(X6, np.array([[u, v]]))
+        dd = x - p[0]
+        d = math.sqrt(ddot3(dd, dd))
+        if d < best:
+            best, local = d, mesh.circumradii[t]
+    return float(best), float(local)
+
+
+_DPA = ((), (1 / 5,), (3 / 40, 9 / 40), (44 / 45, -56 / 15, 32 / 9),
+        (19372 / 6561, -25360 / 2187, 64448 / 6561, -212 / 729),
+        (9017 / 3168, -355 / 33, 46732 / 5247, 49 / 176, -5103 / 18656),
+        (35 / 384, 0.0, 500 / 1113, 125 / 192, -2187 / 6784, 11 / 84))
+_DPB5 = np.array([35 / 384, 0.0, 500 / 1113, 125 / 192, -2187 / 6784, 11 / 84, 0.0])
+_DPB4 = np.array([5179 / 57600, 0.0, 7571 / 16695, 393 / 640, -92097 / 339200, 187 / 2100, 1 / 40])
+
+
+def trace_line(mesh, u, start, orientation=1, rel_tol=1e-6, h_min_frac=1e-6, h_max_frac=0.05, surface_tol_frac=0.1,
+               e_floor=0.0, max_length_frac=4.0, bbox_factor=1.5, cfg=None, efield=None):
+    """Dormand-Prince 5(4) on the unit tangent (postprocess.py:244-357).
+    Returns (points (m,3), |E| (m,), arcs (m,), termination).  ``efield``
+    overrides the field evaluator (default: oracle kernel rows)."""
+    ev = efield or (lambda p: efield_points(mesh, u, p[None], cfg)[0])
+    lo, hi = mesh.vertices.min(axis=0), mesh.vertices.max(axis=0)
+    center, half = 0.5 * (lo + hi), 0.5 * (hi - lo) * bbox_factor
+    diag = math.sqrt(ddot3(hi - lo, hi - lo))
+    h_min, h_max, l_max = h_min_frac * diag, h_max_frac * diag, max_length_frac * diag
+    sign = 1.0 if orientation >= 0 else -1.0
+
+    def tangent(p):
+        e = ev(p)
+        mag = math.sqrt(ddot3(e, e))
+        if mag <= e_floor or mag == 0.0:
+            return None, mag
+        return sign * e / mag, mag
+
+    x = np.asarray(start, dtype=float)
+    t0, mag0 = tangent(x)
+    if t0 is None:
+        raise ValueError("weak field at the start point")
+    pts, mags, arcs = [x.copy()], [mag0], [0.0]
+    term, h, s, k1, armed = "MaxLength", h_max, 0.0, t0, False
+    while True:
+        d_surf, local_r = surface_distance(mesh, x)
+        hit = surface_tol_frac * local_r
+        if d_surf > 2.0 * hit:
+            armed = True
+        if armed and d_surf < hit:
+            term = "SurfaceHit"
+            xe = x + k1 * d_surf
+            pts[-1] = xe
+            arcs[-1] += d_surf
+            e = ev(xe)
+            mags[-1] = math.sqrt(ddot3(e, e))
+            break
+        if s >= l_max:
+            break
+        if np.any(np.abs(x - center) > half):
+            term = "LeftDomain"
+            break
+        h_cap = h_max if d_surf > 4.0 * h_max else max(h_min, 0.45 * d_surf)
+        h = min(h, h_cap, l_max - s + h_min)
+        ks, failed = [k1], False
+        for stage in range(1, 7):
+            acc = 0
+            for a, k in zip(_DPA[stage], ks):
+                acc = acc + a * k
+            ti, _ = tangent(x + h * acc)
+            if ti is None:
+                term, failed = "WeakField", True
+                break
+            ks.append(ti)
+        if failed:
+            break
+        K = np.array(ks)
+        x5, x4 = x + h * (_DPB5 @ K), x + h * (_DPB4 @ K)
+        dd = x5 - x4
+        err = math.sqrt(ddot3(dd, dd))
+        tol = rel_tol * max(1.0, math.sqrt(ddot3(x5, x5)) / diag) * diag
+        if err <= tol or h <= h_min * 1.0000001:
+            x, s = x5, s + h
+            t_new, mag_new = tangent(x)
+            pts.append(x.copy())
+            mags.append(mag_new)
+            arcs.append(s)
+            if t_new is None:
+                term = "WeakField"
+                break
+            k1 = t_new
+        factor = 0.9 * (tol / err) ** 0.2 if err > 0.0 else 2.0
+        h = float(np.clip(h * np.clip(factor, 0.2, 2.0), h_min, h_max))
+    return np.array(pts), np.array(mags), np.array(arcs), term

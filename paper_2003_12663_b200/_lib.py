@@ -37,6 +37,11 @@ SIGNATURES = {
     "hvb_field_reduce": [_P, _I, _I, _P, _P],
     "hvb_near_apply_points": [_P, _I, _P, _P, _P, _P, _I, _P, _P],
     "hvb_field_singular": [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P, _D, _P, _P, _P],
+    "hvb_trace_ctrl": [_P, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P],
+    "hvb_trace_summary": [_P, _I, _P, _P, _P],
+    "hvb_surface_distance": [_P, _I, _P, _I, _P, _P, _P],
+    "hvb_near_coincide": [_P, _LL, _P, _P, _D, _P, _P],
+    "hvb_streamer": [_P, _P, _I, _I, _P, _P, _I, _D, _P, _P, _P],
     "hvb_bench_dfma": [_P, _I, _I, _P],
     "hvb_bench_latency": [_P, _I, _P],
     "hvb_bench_nodes": [_P, _I, _I, _I, _I, _P],
@@ -77,6 +82,8 @@ def lib():
             h.hvb_last_error.restype = ctypes.c_char_p
             h.hvb_last_error.argtypes = []
             h.hvb_version.restype = _I
+            h.hvb_line_state_bytes.restype = _I
+            h.hvb_line_state_bytes.argtypes = []
             _lib = h
     return _lib
 

@@ -205,4 +205,68 @@ int hvb_field_singular(const double* nodes6, const int* tri_cols, const int* vc_
                "hvb_field_singular");
 }
 
+int hvb_line_state_bytes(void) { return (int)sizeof(hvb::LineState); }
+
+int hvb_trace_ctrl(void* state, int n_lines, const double* starts, const int* orient, const double* geo, int mode,
+                   double* e_pts, int* e_line, double* sd_pts, int* sd_line, unsigned long long* counters,
+                   const double* e_out, const int* e_flag, const double* sd_out, double* out_pts,
+                   int cap, void* stream) {
+  if (n_lines < 0 || mode < 0 || mode > 2 || cap < 2) return fail(HVB_EARG, "hvb_trace_ctrl: bad n_lines/mode/cap");
+  if (mode == 0 && (!starts || !orient)) return fail(HVB_EARG, "hvb_trace_ctrl: init needs starts and orientations");
+  hvb::TraceArgs a;
+  a.state = static_cast<hvb::LineState*>(state);
+  a.n_lines = n_lines;
+  a.starts = starts;
+  a.orient = orient;
+  for (int d = 0; d < 3; ++d) {
+    a.center[d] = geo[d];
+    a.half[d] = geo[3 + d];
+  }
+  a.diag = geo[6];
+  a.h_min = geo[7];
+  a.h_max = geo[8];
+  a.l_max = geo[9];
+  a.rel_tol = geo[10];
+  a.tol_frac = geo[11];
+  a.e_floor = geo[12];
+  a.e_pts = e_pts;
+  a.e_line = e_line;
+  a.sd_pts = sd_pts;
+  a.sd_line = sd_line;
+  a.counters = counters;
+  a.e_out = e_out;
+  a.e_flag = e_flag;
+  a.sd_out = sd_out;
+  a.out_pts = out_pts;
+  a.cap = cap;
+  return check(hvb::launch_trace_ctrl(a, mode, (cudaStream_t)stream), "hvb_trace_ctrl");
+}
+
+int hvb_trace_summary(const void* state, int n_lines, int* info, double* dinfo, void* stream) {
+  return check(hvb::launch_trace_summary(static_cast<const hvb::LineState*>(state), n_lines, info, dinfo,
+                                         (cudaStream_t)stream),
+               "hvb_trace_summary");
+}
+
+int hvb_surface_distance(const double* pts, int m, const double* ccr, int nt, const double* nodes6, double* out,
+                         void* stream) {
+  if (m < 0 || nt < 1) return fail(HVB_EARG, "hvb_surface_distance: bad m/nt");
+  return check(hvb::launch_surface_distance(pts, m, ccr, nt, nodes6, out, (cudaStream_t)stream),
+               "hvb_surface_distance");
+}
+
+int hvb_near_coincide(const int* pairs, long long n_pairs, const double* pts, const double* nodes6, double prox,
+                      int* flag, void* stream) {
+  return check(hvb::launch_near_coincide(pairs, n_pairs, pts, nodes6, prox, flag, (cudaStream_t)stream),
+               "hvb_near_coincide");
+}
+
+int hvb_streamer(const double* out_pts, const void* state, int n_lines, int cap, const double* e_tab,
+                 const double* a_tab, int n_tab, double k_str, double* value, int* verdict, void* stream) {
+  if (n_tab < 1) return fail(HVB_EARG, "hvb_streamer: empty ionization table");
+  return check(hvb::launch_streamer(out_pts, static_cast<const hvb::LineState*>(state), n_lines, cap, e_tab, a_tab,
+                                    n_tab, k_str, value, verdict, (cudaStream_t)stream),
+               "hvb_streamer");
+}
+
 }  // extern "C"

@@ -107,4 +107,50 @@ cudaError_t launch_field_singular(const double* nodes6, const int* tri_cols, con
                                   const double* normals, const int* own_col, int m, const double* u, double side,
                                   double* efield, double* emag, cudaStream_t st);
 
+// ---- device tracer (trace.cu) ----
+constexpr int kPhaseStart = 0, kPhaseSD = 1, kPhaseStage = 2, kPhaseAccept = 3, kPhaseSnap = 4, kPhaseDone = 5;
+constexpr int kSurfaceHit = 0, kWeakField = 1, kMaxLength = 2, kLeftDomain = 3;
+constexpr int kStatusRunning = 0, kStatusDone = 1, kStatusWeakStart = 2, kStatusCoincident = 3;
+
+struct LineState {        // 304 bytes, one per line, in HBM
+  double x[3];            // current point
+  double k[7][3];         // stage tangents (k[0] = FSAL k1)
+  double req[3];          // outstanding E request point
+  double h, s, err, tol, d_surf, local_r, sign;
+  int phase, stage, npts, armed, term, status, slot, pad;
+};
+
+struct TraceArgs {
+  LineState* state;
+  int n_lines;
+  const double* starts;   // (n_lines, 3)
+  const int* orient;      // (n_lines)
+  // geometry / parameters (reference trace_fieldline 258-268, TraceParams)
+  double center[3], half[3];
+  double diag, h_min, h_max, l_max, rel_tol, tol_frac, e_floor;
+  // request lists (compacted by atomics): E requests, SD requests
+  double* e_pts;          // (n_lines, 3)
+  int* e_line;
+  double* sd_pts;         // (n_lines, 3)
+  int* sd_line;
+  unsigned long long* counters;  // [0] E requests, [1] SD requests, [2] max points per line
+  // results of the previous requests
+  const double* e_out;    // (n_req, 3)
+  const int* e_flag;      // (n_req) 1 = coincident with a mesh vertex
+  const double* sd_out;   // (n_sd, 2) d_surf, local R
+  // polylines: (n_lines, cap, 5) x, y, z, |E|, s
+  double* out_pts;
+  int cap;
+};
+
+cudaError_t launch_trace_ctrl(const TraceArgs& a, int mode, cudaStream_t st);
+cudaError_t launch_surface_distance(const double* pts, int m, const double* ccr, int nt, const double* nodes6,
+                                    double* out, cudaStream_t st);
+cudaError_t launch_near_coincide(const int* pairs, long long n_pairs, const double* pts, const double* nodes6,
+                                 double prox, int* flag, cudaStream_t st);
+cudaError_t launch_trace_summary(const LineState* state, int n_lines, int* info, double* dinfo, cudaStream_t st);
+cudaError_t launch_streamer(const double* out_pts, const LineState* state, int n_lines, int cap, const double* e_tab,
+                            const double* a_tab, int n_tab, double k_str, double* value, int* verdict,
+                            cudaStream_t st);
+
 }  // namespace hvb

@@ -17,8 +17,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _fp, _lib
-from .mesh import SurfaceMesh, map_reference
-from .quadrature import QuadConfig, closest_point_flat
+from .mesh import SurfaceMesh
+from .quadrature import QuadConfig
 
 __all__ = [
     "IonizationModel",
@@ -156,8 +156,17 @@ def _u_device(solution, dm):
     return hit[1], hit[0]
 
 
-def field_points_device(dm, u_dev, src, X_dev, potential: bool, own_col=None):
-    """(m, 3) field (or potential in column 0) at device points X_dev (m,3)."""
+def panel_split(nt: int) -> int:
+    """Panel-range split of the N-body launch (grid.y).  A function of the
+    mesh only, so every target's sum has the same order whatever the batch
+    (results independent of batch size and GPU count)."""
+    return int(max(1, min(64, nt // 1024)))
+
+
+def field_points_device(dm, u_dev, src, X_dev, potential: bool, own_col=None, coincide_flag=None):
+    """(m, 3) field (or potential in column 0) at device points X_dev (m,3).
+    ``coincide_flag`` (m,) int32: set to 1 for targets within
+    VERTEX_PROXIMITY of a node of one of their near panels."""
     import torch
 
     dev = dm.device
@@ -166,9 +175,7 @@ def field_points_device(dm, u_dev, src, X_dev, potential: bool, own_col=None):
     out = torch.zeros((m, 3), dtype=torch.float64, device=dev)
     if m == 0:
         return out
-    ctas = -(-m // 128)
-    split = int(max(1, min(64, -(-4 * 148 // ctas))))
-    split = min(split, max(1, dm.nt // 32))
+    split = panel_split(dm.nt)
     part = torch.empty((split, m, 4), dtype=torch.float64, device=dev)
     cap = max(4096, 8 * m)
     while True:
@@ -194,6 +201,9 @@ def field_points_device(dm, u_dev, src, X_dev, potential: bool, own_col=None):
                   _lib.ptr(dm.radii), _lib.ptr(dm.rule_near), len(dm.rule_near), _lib.ptr(dm.rule_graded),
                   len(dm.rule_graded), int(dm.cfg.bisect_depth), float(dm.cfg.bisect_trigger),
                   _lib.ptr(contrib), s)
+        if coincide_flag is not None:
+            _lib.call("hvb_near_coincide", _lib.ptr(pairs), n_near, _lib.ptr(X_dev), _lib.ptr(dm.nodes6),
+                      VERTEX_PROXIMITY, _lib.ptr(coincide_flag), s)
         seg = _segments(pairs[:, 0])
         _lib.call("hvb_near_apply_points", _lib.ptr(seg), len(seg) - 1, _lib.ptr(pairs), _lib.ptr(contrib),
                   _lib.ptr(dm.tri_cols), _lib.ptr(u_dev), int(potential), _lib.ptr(out), s)
@@ -265,32 +275,26 @@ def surface_field_magnitudes(mesh: SurfaceMesh, solution, cfg: QuadConfig | None
 # ---------------------------------------------------------------------------
 
 
+def surface_distance_batch(mesh: SurfaceMesh, X, cfg: QuadConfig | None = None):
+    """(d_surf (m,), local circumradius (m,)) at many points on the device
+    (reference _surface_distance, src/postprocess.py:198-218, per point)."""
+    import torch
+
+    from .device import device_mesh
+    from .tracer import surface_distance_device
+
+    dm = device_mesh(mesh, cfg or QuadConfig())
+    X = np.ascontiguousarray(np.asarray(X, dtype=np.float64).reshape(-1, 3))
+    out = surface_distance_device(dm, torch.as_tensor(X, device=dm.device)).cpu().numpy()
+    return out[:, 0].copy(), out[:, 1].copy()
+
+
 def _surface_distance(mesh: SurfaceMesh, x: np.ndarray, candidates: int = 12):
-    d_cc = _fp.norm3_axis(mesh.circumcenters - x[None, :])
-    lower = d_cc - mesh.circumradii
-    if len(lower) > 4 * candidates:
-        part = np.argpartition(lower, candidates)[:candidates]
-        order = part[np.argsort(lower[part], kind="stable")]
-    else:
-        order = np.argsort(lower, kind="stable")[:candidates]
-    best = np.inf
-    local_r = mesh.circumradii[order[0]]
-    for ti in order:
-        corners = mesh.tri_nodes[ti, :3]
-        u, v = closest_point_flat(x, corners)
-        p = map_reference(_TriView(mesh, ti), np.array([u, v]))
-        d = float(_fp.norm3_fused(x - p))
-        if d < best:
-            best = d
-            local_r = mesh.circumradii[ti]
-    return float(best), float(local_r)
-
-
-class _TriView:
-    __slots__ = ("nodes",)
-
-    def __init__(self, mesh, ti):
-        self.nodes = mesh.tri_nodes[ti]
+    """Reference src/postprocess.py:198-218 for one point (device kernel)."""
+    if candidates != 12:
+        raise ValueError("the device surface distance ranks 12 candidates (reference default)")
+    d, r = surface_distance_batch(mesh, np.asarray(x, dtype=float)[None])
+    return float(d[0]), float(r[0])
 
 
 def _local_circumradius(mesh: SurfaceMesh, x: np.ndarray) -> float:
@@ -303,9 +307,11 @@ def pick_start_points(mesh: SurfaceMesh, solution, k: int, offset_frac: float = 
     if surface_e is None:
         surface_e = surface_field_magnitudes(mesh, solution, cfg=cfg)
     order = np.argsort(surface_e)[::-1][:k]
-    starts = [mesh.colloc_points[i] + offset_frac * _local_circumradius(mesh, mesh.colloc_points[i])
-              * mesh.colloc_normals[i] for i in order]
-    return np.array(starts), order, surface_e
+    if len(order) == 0:
+        return np.zeros((0, 3)), order, surface_e
+    _, local = surface_distance_batch(mesh, mesh.colloc_points[order], cfg)
+    starts = mesh.colloc_points[order] + (offset_frac * local)[:, None] * mesh.colloc_normals[order]
+    return starts, order, surface_e
 
 
 # ---------------------------------------------------------------------------

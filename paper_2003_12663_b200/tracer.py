@@ -1,181 +1,225 @@
-"""Batched Dormand-Prince field-line tracer (reference trace_fieldline,
-src/postprocess.py:244-357).
+"""Device-resident Dormand-Prince field-line tracer (reference
+trace_fieldline, src/postprocess.py:244-357; surface distance 198-218;
+streamer integral 365-374).
 
-Every line is a small state machine (a generator) that yields the points
-where it needs E; the driver gathers the requests of all live lines into
-ONE batched device evaluation per round (lockstep over lines), so the
-device sees (#live lines)-point N-body launches instead of one launch per
-stage per line.  The control logic -- stage points, error norm, accept /
-reject, step control, surface-hit arming and snapping, termination order --
-is the reference's, evaluated in the same floating-point order.
+Every line is a state machine in HBM (csrc/trace.cu, ``LineState``).  The
+host drives *rounds*; per round it launches
+
+    k_trace_ctrl(mode=1)      consume E at each live line's last request
+    k_surface_distance        lines that need d_surf(x) (once per step)
+    k_trace_ctrl(mode=2)      consume d_surf, issue the next E request
+    field N-body (field.cu)   ONE batched evaluation over all requests
+                              (+ deferred near pairs, vertex-coincidence flags)
+
+and reads back three counters (E requests, SD requests, longest polyline).
+Lines therefore advance in lockstep, one field evaluation per round, and
+the control arithmetic -- stage points, error norm, accept / reject, step
+control, surface-hit arming and snapping, termination order -- is the
+reference's, statement by statement, on the device.
 """
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
+import ctypes
+import os
+
 import numpy as np
 
-from . import _fp
-from .postprocess import (
-    LEFT_DOMAIN,
-    MAX_LENGTH,
-    SURFACE_HIT,
-    WEAK_FIELD,
-    FieldLine,
-    TraceError,
-    _DP_A,
-    _DP_B4,
-    _DP_B5,
-    _surface_distance,
-)
+from . import _fp, _lib
+
+TERMINATIONS = ("SurfaceHit", "WeakField", "MaxLength", "LeftDomain")
+STATUS_RUNNING, STATUS_DONE, STATUS_WEAK_START, STATUS_COINCIDENT = 0, 1, 2, 3
+VERTEX_PROXIMITY = 1e-12
+_LOG = int(os.environ.get("HVB_TRACE_LOG", "0"))  # print progress every N rounds
 
 
-class _Coincident:
-    """Marker result for an E request at a mesh vertex (ValueError)."""
+@dataclass
+class TraceResult:
+    """Device polylines of a traced batch (torch tensors on the device)."""
+
+    polylines: object   # (L, cap, 5): x, y, z, |E|, s
+    info: np.ndarray    # (L, 4): npts, termination code, status, phase
+    start_mag: np.ndarray
+    state: object
+    cap: int
+    rounds: int
+    field_points: int   # total E evaluations
+
+    @property
+    def n_lines(self) -> int:
+        return len(self.info)
 
 
-def _line(x0, sign, p, geo, mesh):
-    """Generator: yields a point, receives E (3,) or _Coincident."""
-    center, half, diag, h_min, h_max, l_max = geo
-
-    def tangent(e):
-        mag = float(_fp.norm3_fused(e))
-        if mag <= p.e_floor or mag == 0.0:
-            return None, mag
-        return sign * e / mag, mag
-
-    x = np.asarray(x0, dtype=float)
-    e = yield x
-    if isinstance(e, _Coincident):
-        raise ValueError("evaluation point coincides with a mesh vertex")
-    t0, mag0 = tangent(e)
-    if t0 is None:
-        raise TraceError(
-            f"|E| = {mag0:.3e} V/m at the start point is not above the weak-field floor {p.e_floor:.3e}"
-        )
-    points = [x.copy()]
-    mags = [mag0]
-    arcs = [0.0]
-    term = MAX_LENGTH
-    h = h_max
-    s = 0.0
-    k1 = t0
-    armed = False
-    while True:
-        d_surf, local_r = _surface_distance(mesh, x)
-        hit_tol = p.surface_tol_frac * local_r
-        if d_surf > 2.0 * hit_tol:
-            armed = True
-        if armed and d_surf < hit_tol:
-            term = SURFACE_HIT
-            x_end = x + k1 * d_surf
-            points[-1] = x_end
-            arcs[-1] += d_surf
-            e = yield x_end
-            if not isinstance(e, _Coincident):
-                mags[-1] = float(_fp.norm3_fused(e))
-            break
-        if s >= l_max:
-            term = MAX_LENGTH
-            break
-        if np.any(np.abs(x - center) > half):
-            term = LEFT_DOMAIN
-            break
-        h_cap = h_max if d_surf > 4.0 * h_max else max(h_min, 0.45 * d_surf)
-        h = min(h, h_cap, l_max - s + h_min)
-        ks = [k1]
-        failed = False
-        for stage in range(1, 7):
-            acc = 0
-            for a, k in zip(_DP_A[stage], ks):
-                acc = acc + a * k
-            xi = x + h * acc
-            e = yield xi
-            if isinstance(e, _Coincident):
-                raise ValueError("evaluation point coincides with a mesh vertex")
-            ti, _ = tangent(e)
-            if ti is None:
-                term = WEAK_FIELD
-                failed = True
-                break
-            ks.append(ti)
-        if failed:
-            break
-        K = np.array(ks)
-        x5 = x + h * (_DP_B5 @ K)
-        x4 = x + h * (_DP_B4 @ K)
-        err = float(_fp.norm3_fused(x5 - x4))
-        tol = p.rel_tol * max(1.0, float(_fp.norm3_fused(x5)) / diag) * diag
-        if err <= tol or h <= h_min * 1.0000001:
-            x = x5
-            s += h
-            e = yield x
-            if isinstance(e, _Coincident):
-                raise ValueError("evaluation point coincides with a mesh vertex")
-            t_new, mag_new = tangent(e)
-            if t_new is None:
-                points.append(x.copy())
-                mags.append(mag_new)
-                arcs.append(s)
-                term = WEAK_FIELD
-                break
-            k1 = t_new
-            points.append(x.copy())
-            mags.append(mag_new)
-            arcs.append(s)
-        factor = 0.9 * (tol / err) ** 0.2 if err > 0.0 else 2.0
-        h = float(np.clip(h * np.clip(factor, 0.2, 2.0), h_min, h_max))
-    return FieldLine(points=np.array(points), e_magnitudes=np.array(mags), arc_lengths=np.array(arcs),
-                     termination=term)
-
-
-def trace_batch(solution, mesh, starts, orientations, params, cfg, raise_weak=False):
-    import torch
-
-    from .device import device_mesh
-    from .postprocess import _check_points, _sources, _u_device, field_points_device
-
+def _geometry(mesh, params):
     lo, hi = mesh.bounding_box()
     center = 0.5 * (lo + hi)
     half = 0.5 * (hi - lo) * params.bbox_factor
     diag = float(_fp.norm3_fused(hi - lo))
-    geo = (center, half, diag, params.h_min_frac * diag, params.h_max_frac * diag, params.max_length_frac * diag)
+    geo = np.concatenate([center, half, [diag, params.h_min_frac * diag, params.h_max_frac * diag,
+                                         params.max_length_frac * diag, params.rel_tol, params.surface_tol_frac,
+                                         params.e_floor]])
+    return geo.astype(np.float64)
+
+
+def surface_distance_device(dm, X_dev):
+    """(m, 2) = (d_surf, local circumradius) at device points (K12)."""
+    import torch
+
+    m = int(X_dev.shape[0])
+    out = torch.empty((m, 2), dtype=torch.float64, device=dm.device)
+    if m:
+        _lib.call("hvb_surface_distance", _lib.ptr(X_dev), m, _lib.ptr(dm.ccr), dm.nt, _lib.ptr(dm.nodes6),
+                  _lib.ptr(out), _lib.stream_ptr(dm.device))
+    return out
+
+
+def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap: int = 64,
+                 max_rounds: int | None = None) -> TraceResult:
+    import torch
+
+    from .device import device_mesh
+    from .postprocess import _sources, _u_device, field_points_device
+
     dm = device_mesh(mesh, cfg)
+    dev = dm.device
+    st = _lib.stream_ptr(dev)
     u_dev, key = _u_device(solution, dm)
     src = _sources(dm, u_dev, key)
+    starts = np.ascontiguousarray(np.asarray(starts, dtype=np.float64).reshape(-1, 3))
+    L = len(starts)
+    orient = np.asarray(orientations, dtype=np.float64).reshape(-1)
+    if orient.shape != (L,):
+        raise ValueError(f"{L} start points but {orient.size} orientations")
+    f64 = dict(dtype=torch.float64, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    sbytes = _lib.lib().hvb_line_state_bytes()
+    state = torch.zeros(max(1, L) * sbytes, dtype=torch.uint8, device=dev)
+    geo = np.ascontiguousarray(_geometry(mesh, params))  # host parameters (13 doubles)
+    geo_p = geo.ctypes.data_as(ctypes.c_void_p)
+    starts_d = torch.as_tensor(starts, **f64)
+    orient_d = torch.as_tensor(np.where(orient >= 0, 1, -1).astype(np.int32), **i32)
+    cap = max(2, int(initial_cap))
+    poly = torch.empty((max(1, L), cap, 5), **f64)
+    n = max(1, L)
+    e_pts = [torch.empty((n, 3), **f64), torch.empty((n, 3), **f64)]
+    e_line = [torch.empty(n, **i32), torch.empty(n, **i32)]
+    sd_pts = torch.empty((n, 3), **f64)
+    sd_line = torch.empty(n, **i32)
+    sd_out = torch.empty((n, 2), **f64)
+    e_out = torch.empty((n, 3), **f64)
+    e_flag = torch.zeros(n, **i32)
+    counters = torch.zeros(3, dtype=torch.int64, device=dev)
 
-    starts = np.asarray(starts, dtype=float).reshape(-1, 3)
-    gens = []
-    pending = {}
-    results = [None] * len(starts)
-    for i, (x0, o) in enumerate(zip(starts, orientations)):
-        g = _line(x0, 1.0 if o >= 0 else -1.0, params, geo, mesh)
-        gens.append(g)
-        pending[i] = next(g)
-    while pending:
-        idx = list(pending)
-        X = np.array([pending[i] for i in idx])
-        # coincidence check per request (reference raises inside eval_efield)
-        bad = set()
-        for j, i in enumerate(idx):
-            try:
-                _check_points(mesh, X[j:j + 1])
-            except ValueError:
-                bad.add(j)
-        ok = [j for j in range(len(idx)) if j not in bad]
-        E = np.zeros((len(idx), 3))
-        if ok:
-            Xd = torch.as_tensor(np.ascontiguousarray(X[ok]), device=dm.device)
-            E[ok] = field_points_device(dm, u_dev, src, Xd, False).cpu().numpy()
-        nxt = {}
-        for j, i in enumerate(idx):
-            val = _Coincident() if j in bad else E[j]
-            try:
-                nxt[i] = gens[i].send(val)
-            except StopIteration as stop:
-                results[i] = stop.value
-            except TraceError:
-                if raise_weak:
-                    raise
-                results[i] = None
-        pending = nxt
-    return results
+    def ctrl(mode, buf):
+        _lib.call("hvb_trace_ctrl", _lib.ptr(state), L, _lib.ptr(starts_d), _lib.ptr(orient_d), geo_p, mode,
+                  _lib.ptr(e_pts[buf]), _lib.ptr(e_line[buf]), _lib.ptr(sd_pts), _lib.ptr(sd_line),
+                  _lib.ptr(counters), _lib.ptr(e_out), _lib.ptr(e_flag), _lib.ptr(sd_out), _lib.ptr(poly), cap, st)
+
+    rounds = 0
+    evals = 0
+    if L:
+        ctrl(0, 0)
+    n_e, cur = L, 0
+    max_pts = 0
+    while n_e > 0 and (max_rounds is None or rounds < max_rounds):
+        rounds += 1
+        evals += n_e
+        # one batched field evaluation over every outstanding request
+        e_flag[:n_e].zero_()
+        E = field_points_device(dm, u_dev, src, e_pts[cur][:n_e], False, coincide_flag=e_flag)
+        e_out[:n_e].copy_(E)
+        if max_pts + 1 >= cap:  # at most one point is appended per line per round
+            new = torch.empty((L, 2 * cap, 5), **f64)
+            new[:, :cap] = poly
+            poly, cap = new, 2 * cap
+        counters.zero_()
+        nxt = 1 - cur
+        ctrl(1, nxt)
+        c = counters.cpu().numpy()
+        if c[1]:
+            sd_out[: c[1]].copy_(surface_distance_device(dm, sd_pts[: c[1]]))
+            ctrl(2, nxt)
+            c = counters.cpu().numpy()
+        n_e, max_pts, cur = int(c[0]), int(c[2]), nxt
+        if _LOG and rounds % _LOG == 0:
+            print(f"[trace] round {rounds}: {n_e} requests, {int(c[1])} surface queries, longest {max_pts} points",
+                  flush=True)
+
+    info = torch.empty((max(1, L), 4), **i32)
+    dinfo = torch.empty(max(1, L), **f64)
+    _lib.call("hvb_trace_summary", _lib.ptr(state), L, _lib.ptr(info), _lib.ptr(dinfo), st)
+    return TraceResult(polylines=poly, info=info[:L].cpu().numpy(), start_mag=dinfo[:L].cpu().numpy(), state=state,
+                       cap=cap, rounds=rounds, field_points=evals)
+
+
+# host view of csrc/launch.cuh LineState (diagnostics only)
+LINE_STATE_DTYPE = np.dtype([("x", "<f8", 3), ("k", "<f8", (7, 3)), ("req", "<f8", 3), ("h", "<f8"), ("s", "<f8"),
+                             ("err", "<f8"), ("tol", "<f8"), ("d_surf", "<f8"), ("local_r", "<f8"), ("sign", "<f8"),
+                             ("phase", "<i4"), ("stage", "<i4"), ("npts", "<i4"), ("armed", "<i4"), ("term", "<i4"),
+                             ("status", "<i4"), ("slot", "<i4"), ("pad", "<i4")])
+
+
+def line_states(res: TraceResult) -> np.ndarray:
+    """Structured host copy of every line's state machine."""
+    raw = res.state.cpu().numpy()
+    return raw.view(LINE_STATE_DTYPE)[: res.n_lines]
+
+
+def streamer_device(res: TraceResult, model):
+    """(values, verdicts) of every traced line on the device (K14)."""
+    import torch
+
+    dev = res.polylines.device
+    L = res.n_lines
+    e_tab = torch.as_tensor(np.asarray(model.e_values, dtype=np.float64), device=dev)
+    a_tab = torch.as_tensor(np.asarray(model.alpha_values, dtype=np.float64), device=dev)
+    val = torch.empty(max(1, L), dtype=torch.float64, device=dev)
+    ver = torch.empty(max(1, L), dtype=torch.int32, device=dev)
+    _lib.call("hvb_streamer", _lib.ptr(res.polylines), _lib.ptr(res.state), L, res.cap, _lib.ptr(e_tab),
+              _lib.ptr(a_tab), len(e_tab), float(model.k_str), _lib.ptr(val), _lib.ptr(ver), _lib.stream_ptr(dev))
+    return val[:L], ver[:L]
+
+
+def raise_for_status(res: TraceResult, params, raise_weak: bool):
+    from .postprocess import TraceError
+
+    st = res.info[:, 2]
+    bad = np.nonzero(st == STATUS_COINCIDENT)[0]
+    if len(bad):
+        raise ValueError(f"evaluation point coincides with a mesh vertex (line {int(bad[0])})")
+    weak = np.nonzero(st == STATUS_WEAK_START)[0]
+    if len(weak) and raise_weak:
+        mag = float(res.start_mag[weak[0]])
+        raise TraceError(
+            f"|E| = {mag:.3e} V/m at the start point is not above the weak-field floor {params.e_floor:.3e}")
+
+
+def field_lines(res: TraceResult) -> list:
+    """FieldLine objects (host copies) for every line; None for lines that
+    could not start (weak field)."""
+    from .postprocess import FieldLine
+
+    L = res.n_lines
+    if L == 0:
+        return []
+    npts = res.info[:, 0]
+    m = int(npts.max()) if L else 0
+    host = res.polylines[:, :max(1, m)].cpu().numpy()
+    out = []
+    for i in range(L):
+        if res.info[i, 2] != STATUS_DONE:
+            out.append(None)
+            continue
+        k = int(npts[i])
+        P = host[i, :k]
+        out.append(FieldLine(points=P[:, :3].copy(), e_magnitudes=P[:, 3].copy(), arc_lengths=P[:, 4].copy(),
+                             termination=TERMINATIONS[int(res.info[i, 1])]))
+    return out
+
+
+def trace_batch(solution, mesh, starts, orientations, params, cfg, raise_weak=False):
+    res = trace_device(solution, mesh, starts, orientations, params, cfg)
+    raise_for_status(res, params, raise_weak)
+    return field_lines(res)
