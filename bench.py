@@ -9,7 +9,9 @@ disconnector-like rod-plane + insulator mesh, 199,104 curved panels,
 N = 99,558 unknowns, dense FP64 system 79 GB (> L2, so no flush needed).
 One step = one pass of the hot path: assemble the dense system (this rank's
 row block), GMRES solve (reference semantics, rel_tol 1e-8; matvec row-block
-sharded + NCCL all-gather), and E at M field points (points split per
+sharded + NCCL all-gather), E at M field points (points split per rank),
+and config 5 on the step's own solution: surface |E|, the top ``--lines``
+seeds, device RK45 field lines with the streamer verdict (lines split per
 rank).  Inputs are resident in HBM for the device-timed value; the ``e2e``
 leg re-runs the pass through the public API from host buffers (mesh arrays
 H2D, u and E D2H inside the timed region).
@@ -46,6 +48,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--scale", type=float, default=1.0, help="mesh resolution scale (1.0 = config 4)")
     ap.add_argument("--points", type=int, default=100_000, help="field points per step (whole job)")
+    ap.add_argument("--lines", type=int, default=8192, help="cfg5 field lines per step (whole job; 0 = skip)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--cpu-rows", type=int, default=24, help="cpu_baseline sample rows")
@@ -268,7 +271,8 @@ def run_b200(args):
     import __graft_entry__
 
     __graft_entry__.build()
-    from paper_2003_12663_b200 import _lib, assembly, fixtures, postprocess
+    from paper_2003_12663_b200 import _lib, assembly, fixtures, postprocess, tracer
+    from paper_2003_12663_b200.quadrature import QuadConfig
     from paper_2003_12663_b200.assembly import assemble
     from paper_2003_12663_b200.device import device_mesh
     from paper_2003_12663_b200.parallel import assemble_distributed, split_range
@@ -300,9 +304,29 @@ def run_b200(args):
 
     _lib.call = counting_call
 
+    gas = postprocess.load_ionization_model(os.path.join(ROOT, "paper_2003_12663_b200", "data", "air_demo.gas"))
+    trace_stats = {}
+
+    def trace_phase(sol):
+        """cfg5: seeds = top-k surface |E| (orientation sign(E.n), the CLI's
+        rule), lines split per rank, device tracer + streamer verdicts."""
+        if args.lines <= 0:
+            return
+        se = postprocess.surface_field_magnitudes(mesh, sol)
+        starts, idx, _ = postprocess.pick_start_points(mesh, sol, args.lines, surface_e=se)
+        la, lb = split_range(len(starts), world, rank)
+        E0 = postprocess.eval_efield_batch(sol, mesh, starts[la:lb])
+        orient = np.where(np.einsum("ij,ij->i", E0, mesh.colloc_normals[idx[la:lb]]) >= 0, 1, -1)
+        res = tracer.trace_device(sol, mesh, starts[la:lb], orient, postprocess.TraceParams(), QuadConfig())
+        val, ver = tracer.streamer_device(res, gas)
+        trace_stats.update(rounds=res.rounds, evals=res.field_points, lines=lb - la,
+                           inception=int(ver.sum().item()),
+                           terms=np.bincount(res.info[:, 1], minlength=4).tolist(),
+                           max_points=int(res.info[:, 0].max()) if lb > la else 0)
+
     def one_step(profile=None):
         assembly.PROFILE = profile
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         ev[0].record()
         if world > 1:
             A, rhs = assemble_distributed(mesh)
@@ -317,9 +341,11 @@ def run_b200(args):
         src = postprocess._sources(dm, u_dev, key)
         E = postprocess.field_points_device(dm, u_dev, src, P_dev, False)
         ev[3].record()
-        torch.cuda.synchronize(dev)
         del A, E
-        ph = [ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(3)]
+        trace_phase(sol)
+        ev[4].record()
+        torch.cuda.synchronize(dev)
+        ph = [ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(4)]
         return ph, sol
 
     device_mesh(mesh)  # per-mesh setup (tables, tiling, panel streams) outside the timed region
@@ -349,10 +375,15 @@ def run_b200(args):
     total = t_start.elapsed_time(t_end) / 1e3
     ph = np.array(phases).mean(axis=0)
     reg_t = sum(e0.elapsed_time(e1) for lab, e0, e1 in prof if lab == "regular") / 1e3
-    vec = torch.tensor([total, ph[0], ph[1], ph[2], reg_t], dtype=torch.float64, device=dev)
+    vec = torch.tensor([total, ph[0], ph[1], ph[2], ph[3], reg_t], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vec, op=dist.ReduceOp.MAX)
-    total, t_asm, t_solve, t_field, reg_t = vec.tolist()
+    total, t_asm, t_solve, t_field, t_trace, reg_t = vec.tolist()
+    tvec = torch.tensor([trace_stats.get("evals", 0), trace_stats.get("inception", 0)], dtype=torch.float64,
+                        device=dev)
+    if world > 1:
+        dist.all_reduce(tvec)
+    trace_evals, trace_inception = tvec.tolist()
 
     # algorithmic flops of this rank's regular sweep (max-over-ranks time -> rank-0 share x world)
     a, b = split_range(N, world, rank)
@@ -446,7 +477,15 @@ def run_b200(args):
             "gmres_solve_s": t_solve,
             "gmres_iterations": iters,
             "field_evals_per_s": args.points / t_field,
-            "phases_s": {"assembly": t_asm, "solve": t_solve, "field": t_field, "assembly_regular_kernel": reg_t},
+            "phases_s": {"assembly": t_asm, "solve": t_solve, "field": t_field, "trace": t_trace,
+                         "assembly_regular_kernel": reg_t},
+            "trace": {"lines": min(args.lines, n), "lines_per_s": min(args.lines, n) / t_trace if t_trace else None,
+                      "field_evals": int(trace_evals), "inception_lines": int(trace_inception),
+                      "rank0_rounds": trace_stats.get("rounds"), "rank0_terminations": dict(zip(
+                          ("SurfaceHit", "WeakField", "MaxLength", "LeftDomain"), trace_stats.get("terms", []))),
+                      "rank0_max_points": trace_stats.get("max_points"),
+                      "note": "cfg5 on the step's own solution: surface |E|, top-k seeds, sign(E.n) orientation, "
+                              "device RK45 tracer + streamer (air_demo.gas)"},
             "roofline": {"bound": "fp64", "kernel": "k_assemble_regular", "achieved": achieved,
                          "peak": tflops_peak, "unit": "TFLOP/s", "frac": achieved / tflops_peak if tflops_peak else None,
                          "traffic": _ncu_traffic(), "peak_source": "measured DFMA kernel on this GPU (hvb_bench_dfma)"},

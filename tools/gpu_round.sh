@@ -1,14 +1,14 @@
 #!/bin/bash
-# One GPU session: tests, bench line, ncu launch list and full-set captures (dev tool).
-set -x
-python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/pytest_gpu.log
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --points 10000 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_assemble_dual -c 2 -o gpurun_out/prof_dual_full \
-    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --points 10000 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_gemv -c 1 -o gpurun_out/prof_gemv \
-    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --points 10000 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_field -c 1 -o gpurun_out/prof_field \
-    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --points 100000 > /dev/null 2>&1
+# One GPU session (dev tool): tests, bench line, ncu launch list of OUR kernels
+# and full-set captures of the top kernels.  Every step has its own timeout.
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/pytest_gpu.log
+timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ --csv \
+    --log-file gpurun_out/launches.csv \
+    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --points 10000 --lines 1024 > gpurun_out/ncu_launch.log 2>&1
+for k in k_assemble_dual k_gemv k_field k_surface_distance; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o gpurun_out/prof_$k \
+      python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --points 10000 --lines 1024 > gpurun_out/ncu_$k.log 2>&1
+done
 ls -la gpurun_out
