@@ -157,6 +157,7 @@ def regular_flops(mesh, near_rows_counts, sl_rows, adl_rows):
 # ---------------------------------------------------------------------------
 
 _CPU_MESH = None
+EVALS_PER_LINE = 140.2  # field evaluations per traced cfg5 line (B200 run, tools/trace_probe.py 1.0 100000)
 
 
 def _cpu_rows(rows):
@@ -199,21 +200,37 @@ def cpu_sample(mesh, n_rows: int, processes: int, field_points: int = 4):
         blk @ v
     t_mv = (time.perf_counter() - t0) / 3 * (N / blk.shape[0])
     del blk
-    # field evaluation at a few points (1 process)
+    # field evaluation: one point per process (embarrassingly parallel)
     rng = np.random.default_rng(0)
     lo, hi = mesh.bounding_box()
     P = 0.5 * (lo + hi) + rng.uniform(-0.6, 0.6, (field_points, 3)) * (hi - lo)
     t0 = time.perf_counter()
-    ora.efield_points(mesh, np.ones(mesh.n_collocation), P)
+    if processes > 1 and field_points > 1:
+        with mp.get_context("fork").Pool(min(processes, field_points)) as pool:
+            pool.map(_cpu_field, [P[i:i + 1] for i in range(field_points)])
+    else:
+        _cpu_field(P)
     evals_per_s = field_points / (time.perf_counter() - t0)
     return {
         "entries_per_s": entries_per_s,
         "t_rows": t_rows,
         "matvec_s": t_mv,
         "field_evals_per_s": evals_per_s,
+        # a traced line costs ~EVALS_PER_LINE field evaluations (measured on
+        # the B200 cfg5 run; the surface-distance queries are ~1 % on top)
+        "trace_lines_per_s": evals_per_s / EVALS_PER_LINE,
         "sample": (f"oracle port: {n_rows} evenly spaced cfg4 rows (row_equations, {processes} procs) "
-                   f"-> entries/s x N; numpy GEMV on a 4096-row block; E at {field_points} points"),
+                   f"-> entries/s x N; numpy GEMV on a 4096-row block; E at {field_points} points "
+                   f"({min(processes, field_points)} procs); lines/s = evals/s / {EVALS_PER_LINE} (extrapolated)"),
     }
+
+
+def _cpu_field(P):
+    import numpy as np
+
+    from oracle import hvb_oracle as ora
+
+    ora.efield_points(_CPU_MESH, np.ones(_CPU_MESH.n_collocation), P)
 
 
 def run_reference(args):
@@ -230,7 +247,7 @@ def run_reference(args):
     vals = []
     samp = None
     for k in range(args.warmup + args.steps):
-        s = cpu_sample(mesh, max(cores, args.cpu_rows), cores, field_points=2)
+        s = cpu_sample(mesh, max(cores, args.cpu_rows), cores, field_points=max(2, cores))
         if k >= args.warmup:
             vals.append(s)
         samp = s
@@ -245,6 +262,8 @@ def run_reference(args):
                    "N": N},
         "gmres_solve_s": float(np.median([s["matvec_s"] for s in vals])) * (iters + 3),
         "field_evals_per_s": float(np.median([s["field_evals_per_s"] for s in vals])),
+        "trace": {"lines_per_s": float(np.median([s["trace_lines_per_s"] for s in vals])),
+                  "note": "extrapolated: field evals/s / evals per line"},
         "cpu_baseline": {"value": v, "unit": "entries/s", "cores": cores, "kind": "port", "sample": samp["sample"]},
         "e2e": {"value": v, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -454,7 +473,8 @@ def run_b200(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         s = cpu_sample(mesh, args.cpu_rows, 1, field_points=2)
         cpu = {"value": s["entries_per_s"], "unit": "entries/s", "cores": 1, "kind": "port",
-               "sample": s["sample"], "matvec_s": s["matvec_s"], "field_evals_per_s": s["field_evals_per_s"]}
+               "sample": s["sample"], "matvec_s": s["matvec_s"], "field_evals_per_s": s["field_evals_per_s"],
+               "trace_lines_per_s": s["trace_lines_per_s"]}
 
     if rank == 0:
         line = {
@@ -486,10 +506,10 @@ def run_b200(args):
                       "rank0_max_points": trace_stats.get("max_points"),
                       "note": "cfg5 on the step's own solution: surface |E|, top-k seeds, sign(E.n) orientation, "
                               "device RK45 tracer + streamer (air_demo.gas)"},
-            "roofline": {"bound": "fp64", "kernel": "k_assemble_regular", "achieved": achieved,
+            "roofline": {"bound": "fp64", "kernel": "k_assemble_dual", "achieved": achieved,
                          "peak": tflops_peak, "unit": "TFLOP/s", "frac": achieved / tflops_peak if tflops_peak else None,
-                         "traffic": _ncu_traffic(), "peak_source": "measured DFMA kernel on this GPU (hvb_bench_dfma)"},
-            "roofline_gemv": {"bound": "hbm", "kernel": "k_gemv_f64", "achieved": gemv_bytes / t_gemv / 1e9,
+                         "traffic": _ncu_traffic("k_assemble_dual"), "peak_source": "measured DFMA kernel on this GPU (hvb_bench_dfma)"},
+            "roofline_gemv": {"bound": "hbm", "kernel": "k_gemv_f64", "traffic": _ncu_traffic("k_gemv"), "achieved": gemv_bytes / t_gemv / 1e9,
                               "peak": read_gbs, "unit": "GB/s", "frac": gemv_bytes / t_gemv / 1e9 / read_gbs,
                               "frac_of_measured_copy": gemv_bytes / t_gemv / 1e9 / 6547.2,
                               "ms_per_matvec": t_gemv * 1e3,
@@ -517,15 +537,21 @@ def _count_near(mesh, rows):
     return per[rows]
 
 
-def _ncu_traffic():
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        try:
-            with open(p) as fh:
-                return json.load(fh).get("k_assemble_regular_bytes_per_launch")
-        except (OSError, ValueError):
-            return None
-    return None
+def _ncu_traffic(kernel="k_assemble_dual"):
+    """dram read+write bytes of one launch from the newest committed ncu
+    full capture (profiles/rNN_ncu_traffic.json, tools/profile_summary.py)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
+    if not files:
+        return None
+    try:
+        with open(files[-1]) as fh:
+            rec = json.load(fh).get(kernel)
+    except (OSError, ValueError):
+        return None
+    return None if rec is None else {"bytes_per_launch": rec["bytes_per_launch"], "source": os.path.basename(files[-1]),
+                                     "note": "one SL launch of the regular sweep (dominated by the matrix write)"}
 
 
 def main():

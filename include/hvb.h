@@ -169,6 +169,7 @@ int hvb_bench_dfma(double* out, int blocks, int iters, void* stream);
 int hvb_bench_latency(double* out, int n, void* stream);
 int hvb_bench_nodes(double* out, int var, int blocks, int threads, int iters, void* stream);
 int hvb_bench_read(const double* p, long long n, double* out, int blocks, void* stream);
+int hvb_bench_rsqrt(const double* r2, int n, double* out, void* stream);
 
 #ifdef __cplusplus
 }

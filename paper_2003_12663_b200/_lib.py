@@ -46,6 +46,7 @@ SIGNATURES = {
     "hvb_bench_latency": [_P, _I, _P],
     "hvb_bench_nodes": [_P, _I, _I, _I, _I, _P],
     "hvb_bench_read": [_P, _LL, _P, _I, _P],
+    "hvb_bench_rsqrt": [_P, _I, _P, _P],
 }
 
 HVB_EARG = 1

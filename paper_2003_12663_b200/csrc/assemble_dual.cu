@@ -20,9 +20,9 @@
 // decision (common.cuh); non-regular non-singular pairs are emitted once
 // (primary tile) for the deferred near-singular pass.
 //
-// Kernel values: SL uses the MUFU seed + one Newton step (rel. error
-// ~1e-12, entries are sums of positive terms); ADL keeps the cubic step
-// (signed sums, cancellation).
+// Kernel values: SL uses the MUFU seed + one Newton step returning 2/r
+// (rel. error ~1e-12, entries are sums of positive terms; the flush halves
+// exactly); ADL keeps the cubic step (signed sums, cancellation).
 #include "launch.cuh"
 
 namespace hvb {
@@ -85,27 +85,29 @@ __global__ void __launch_bounds__(64) k_assemble_dual(RegularArgs a) {
   const bool flive = fi < a.n_rows;
   const int flr = a.row_begin + (flive ? fi : a.n_rows - 1);
   const int64_t fout = flive ? a.row_out[flr] : -1;
-  const double fscale = a.row_scale[flr];
+  const double fscale = a.row_scale[flr] * (MODE == 0 ? 0.5 : 1.0);  // SL sums hold 2/r (exact halving)
 
   for (int k = lane; k < SLOTS * STRIDE; k += 32) win[k] = 0.0;
 
   const int64_t e0 = a.tile_ptr[tile], e1 = a.tile_ptr[tile + 1];
   const int col0 = a.tile_col0[tile], width = a.tile_width[tile];
   const double* src = a.stream + e0 * REC;
-  const int64_t ne = e1 - e0;
-  const int64_t np = (ne + 1) >> 1;
+  const int ne = (int)(e1 - e0);  // records per tile < 2^31 (host-checked)
+  const int np = (ne + 1) >> 1;
 
-  auto stage = [&](int64_t p) {
-    double* dst = ring + (p % RING) * PREC;
-    const double* s = src + 2 * p * REC;
+  // ring slots advance by one per step (no 64-bit modulo in the loop)
+  auto stage = [&](int p, int slot) {
+    double* dst = ring + slot * PREC;
+    const double* s = src + (size_t)(2 * p) * REC;
     const int nch = (2 * p + 1 < ne) ? REC : REC / 2;
     for (int c = lane; c < nch; c += 32) dual::cp_async16(dst + 2 * c, s + 2 * c);
   };
 #pragma unroll
   for (int s = 0; s < RING - 1; ++s) {
-    if (s < np) stage(s);
+    if (s < np) stage(s, s);
     dual::commit();
   }
+  int cur_slot = 0, nxt_slot = RING - 1;
 
   int base = 0;
   auto flush32 = [&](int b) {
@@ -122,15 +124,17 @@ __global__ void __launch_bounds__(64) k_assemble_dual(RegularArgs a) {
     __syncwarp();
   };
 
-  for (int64_t p = 0; p < np; ++p) {
+  for (int p = 0; p < np; ++p) {
     dual::wait_group<RING - 2>();
     __syncwarp();
-    const double* pr = ring + (p % RING) * PREC;
+    const double* pr = ring + cur_slot * PREC;
     {
-      const int64_t nxt = p + RING - 1;
-      if (nxt < np) stage(nxt);
+      const int nxt = p + RING - 1;
+      if (nxt < np) stage(nxt, nxt_slot);
       dual::commit();
     }
+    cur_slot = cur_slot == RING - 1 ? 0 : cur_slot + 1;
+    nxt_slot = nxt_slot == RING - 1 ? 0 : nxt_slot + 1;
     const int mfirst0 = reinterpret_cast<const int*>(pr + 6 * NQ + 6)[1];
     while (mfirst0 >= base + 32) {
       flush32(base);
@@ -154,9 +158,9 @@ __global__ void __launch_bounds__(64) k_assemble_dual(RegularArgs a) {
       const double r20 = fma(dz0, dz0, fma(dy0, dy0, dx0 * dx0));
       const double r21 = fma(dz1, dz1, fma(dy1, dy1, dx1 * dx1));
       double k0, k1;
-      if (MODE == 0) {
-        k0 = rsqrt_newton(r20);
-        k1 = rsqrt_newton(r21);
+      if (MODE == 0) {  // 2/r: the flush applies the 1/2
+        k0 = rsqrt2_newton(r20);
+        k1 = rsqrt2_newton(r21);
       } else {
         const double ri0 = rsqrt_full(r20);
         const double ri1 = rsqrt_full(r21);

@@ -61,6 +61,16 @@ HVB_DEV double rsqrt_newton(double r2) {
   return __fma_rn(y * 0.5, e, y);
 }
 
+// 2/sqrt(r2): MUFU.RSQ64H seed + one Newton step with the 1/2 folded out,
+// y (3 - r2 y^2) -- 3 FP64 ops.  Callers scale their sums by 1/2 (or 1/8
+// for r^-3) at the end, which is exact.
+HVB_DEV double rsqrt2_newton(double r2) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+  const double h = r2 * y;
+  return y * __fma_rn(-h, y, 3.0);
+}
+
 // Classification "regular iff ||x - cc|| > eta R" exactly as the reference
 // decides it (sqrt of the unfused sum, strict compare against fl(eta*R)).
 // thr = fl(eta*R) and the squared bracket [lo, hi] are precomputed per

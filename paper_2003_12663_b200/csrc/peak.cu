@@ -130,6 +130,21 @@ __global__ void __launch_bounds__(256) k_node_probe(double* out, int iters) {
 
 }  // namespace hvb
 
+namespace hvb {
+__global__ void k_rsqrt_probe(const double* r2, int n, double* out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[2 * i] = rsqrt2_newton(r2[i]);
+  out[2 * i + 1] = rsqrt_full(r2[i]);
+}
+}  // namespace hvb
+
+// accuracy probe of the two rsqrt refinements: out (n, 2) = 2/sqrt, 1/sqrt
+extern "C" int hvb_bench_rsqrt(const double* r2, int n, double* out, void* stream) {
+  hvb::k_rsqrt_probe<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(r2, n, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
 extern "C" int hvb_bench_nodes(double* out, int var, int blocks, int threads, int iters, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (var == 0) hvb::k_node_probe<0><<<blocks, threads, 0, st>>>(out, iters);

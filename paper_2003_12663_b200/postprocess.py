@@ -156,17 +156,45 @@ def _u_device(solution, dm):
     return hit[1], hit[0]
 
 
+PANELS_PER_SPLIT = 512
+
+
 def panel_split(nt: int) -> int:
-    """Panel-range split of the N-body launch (grid.y).  A function of the
-    mesh only, so every target's sum has the same order whatever the batch
-    (results independent of batch size and GPU count)."""
-    return int(max(1, min(64, nt // 1024)))
+    """Panel-range split of the N-body launch (grid.y): chunks of ~512
+    panels.  A function of the mesh only, so every target's sum has the
+    same order whatever the batch (results independent of batch size and
+    GPU count), and small batches (the tracer's tail rounds) still spread
+    over hundreds of CTAs."""
+    return int(max(1, min(4096, -(-nt // PANELS_PER_SPLIT))))
+
+
+TARGET_BATCH = 1 << 17  # targets per launch (bounds the split x m partial buffer)
 
 
 def field_points_device(dm, u_dev, src, X_dev, potential: bool, own_col=None, coincide_flag=None):
     """(m, 3) field (or potential in column 0) at device points X_dev (m,3).
     ``coincide_flag`` (m,) int32: set to 1 for targets within
-    VERTEX_PROXIMITY of a node of one of their near panels."""
+    VERTEX_PROXIMITY of a node of one of their near panels.  Targets are
+    processed in launches of TARGET_BATCH (per-target results do not depend
+    on the batching)."""
+    import torch
+
+    m = int(X_dev.shape[0])
+    if m <= TARGET_BATCH:
+        return _field_points(dm, u_dev, src, X_dev, potential, own_col, coincide_flag)
+    out = torch.empty((m, 3), dtype=torch.float64, device=dm.device)
+    near = 0
+    for a in range(0, m, TARGET_BATCH):
+        b = min(m, a + TARGET_BATCH)
+        part = _field_points(dm, u_dev, src, X_dev[a:b], potential, None if own_col is None else own_col[a:b],
+                             None if coincide_flag is None else coincide_flag[a:b])
+        out[a:b] = part
+        near += part.near_pairs
+    out.near_pairs = near  # type: ignore[attr-defined]
+    return out
+
+
+def _field_points(dm, u_dev, src, X_dev, potential: bool, own_col=None, coincide_flag=None):
     import torch
 
     dev = dm.device

@@ -369,3 +369,15 @@ def test_demo_gas_file_shipped():
 
     m = load_ionization_model(os.path.join(ROOT, "paper_2003_12663_b200", "data", "air_demo.gas"))
     assert m.k_str == 9.15 and len(m.e_values) == 9
+
+
+def test_line_state_layout_matches_library():
+    import ctypes
+
+    import __graft_entry__
+    from paper_2003_12663_b200.tracer import LINE_STATE_DTYPE
+
+    __graft_entry__.build()
+    lib = ctypes.CDLL(__graft_entry__.LIB)
+    lib.hvb_line_state_bytes.restype = ctypes.c_int
+    assert lib.hvb_line_state_bytes() == LINE_STATE_DTYPE.itemsize
