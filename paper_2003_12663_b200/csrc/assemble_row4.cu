@@ -1,0 +1,240 @@
+// Regular sweep (K2+K3), "row4" layout: lane = row (32 rows per warp), FOUR
+// panel records per lane per step (four independent FP64 chains per lane).
+// Unlike the quad layout every lane owns its window row exclusively, so the
+// window adds need no half-warp serialisation; each node's data feeds one
+// row instead of two (twice the shared-memory broadcast loads).  Same
+// record stream, tiling guarantee (groups of 4), classification and
+// summation order as the quad layout.
+#include "launch.cuh"
+
+namespace hvb {
+namespace row4 {
+constexpr int ROWS = 32;
+constexpr int STRIDE = 33;
+constexpr int DEPTH = 2;
+template <int WIN>
+struct Shape {
+  static constexpr int SLOTS = WIN + 1;                    // + dump slot
+  static constexpr int WREG = (SLOTS * STRIDE + 1) & ~1;   // 16-byte aligned region
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// one (row, record) classification: regular iff ||x - cc|| > fl(eta R)
+HVB_DEV bool regular(double sq, const double* cg) {
+  bool r = sq > cg[5];
+  if (!r && !(sq < cg[4])) r = __dsqrt_rn(sq) > cg[3];
+  return r;
+}
+}  // namespace row4
+
+template <int NQ, int MODE, int WIN>
+__global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
+  using namespace row4;
+  constexpr int REC = 6 * NQ + 8;
+  constexpr int SREC = 4 * REC;
+  constexpr int SLOTS = Shape<WIN>::SLOTS;
+  constexpr int WREG = Shape<WIN>::WREG;
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  double* win = smem;
+  double* ring = win + WREG;
+
+  const int rowtile = blockIdx.x;
+  const int tile = blockIdx.y;
+  const int base_row = rowtile * ROWS;
+  if (base_row >= a.n_rows) return;
+
+  const int i0 = base_row + lane;
+  const bool live0 = i0 < a.n_rows;
+  const int lr0 = a.row_begin + (live0 ? i0 : a.n_rows - 1);
+  const double* rd0 = a.rowdata + 6 * (size_t)lr0;
+  const d3 X0 = mk3(rd0[0], rd0[1], rd0[2]);
+  const d3 N0 = mk3(rd0[3], rd0[4], rd0[5]);
+  const bool adl0 = (MODE == 1) || (MODE == 2 && a.row_kind[lr0] == 1);
+  const int own0 = a.row_col[lr0];
+  const int fi = base_row + lane;
+  const bool flive = fi < a.n_rows;
+  const int flr = a.row_begin + (flive ? fi : a.n_rows - 1);
+  const int64_t fout = flive ? a.row_out[flr] : -1;
+  const double fscale = a.row_scale[flr] * (MODE == 0 ? 0.5 : 1.0);  // SL sums hold 2/r (exact halving)
+
+  for (int k = lane; k < SLOTS * STRIDE; k += 32) win[k] = 0.0;
+
+  const int64_t e0 = a.tile_ptr[tile], e1 = a.tile_ptr[tile + 1];
+  const int col0 = a.tile_col0[tile], width = a.tile_width[tile];
+  const double* src = a.stream + e0 * REC;
+  const int ne = (int)(e1 - e0);
+  const int ns = (ne + 3) >> 2;
+
+  auto stage = [&](int p) {
+    double* dst = ring + (p & 1) * SREC;
+    const double* s = src + (size_t)(4 * p) * REC;
+    const int nrec = min(4, ne - 4 * p);
+    const int nch = nrec * (REC / 2);
+    for (int c = lane; c < nch; c += 32) cp_async16(dst + 2 * c, s + 2 * c);
+  };
+  stage(0);
+  commit();
+
+  int base = 0;
+  auto flush32 = [&](int b) {
+    const int c = b + lane;
+    double* wcol = win + (c % WIN) * STRIDE;
+    const bool in = c < width;
+#pragma unroll 8
+    for (int j = 0; j < ROWS; ++j) {
+      const int64_t off = __shfl_sync(0xffffffffu, fout, j);
+      const double sc = __shfl_sync(0xffffffffu, fscale, j);
+      if (off >= 0 && in) a.A[off + col0 + c] = wcol[j] * sc;
+      wcol[j] = 0.0;
+    }
+    __syncwarp();
+  };
+
+  for (int p = 0; p < ns; ++p) {
+    if (p + 1 < ns) stage(p + 1);
+    commit();
+    wait_group<1>();
+    __syncwarp();
+    const double* pr = ring + (p & 1) * SREC;
+    const int mfirst = reinterpret_cast<const int*>(pr + 6 * NQ + 6)[1];
+    while (mfirst >= base + 32) {
+      flush32(base);
+      base += 32;
+    }
+    double acc[4][3];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double* rec = pr + j * REC;
+        const double2 p01 = *reinterpret_cast<const double2*>(rec + 6 * q);
+        const double2 p2w = *reinterpret_cast<const double2*>(rec + 6 * q + 2);
+        const double2 w12 = *reinterpret_cast<const double2*>(rec + 6 * q + 4);
+        const double dx = X0.x - p01.x, dy = X0.y - p01.y, dz = X0.z - p2w.x;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        double k;
+        if (MODE == 0) {  // 2/r: the flush applies the 1/2
+          k = rsqrt2_newton(r2);
+        } else {
+          const double ri = rsqrt_full(r2);
+          const double dn = fma(dz, N0.z, fma(dy, N0.y, dx * N0.x));
+          const double t = dn * (ri * ri * ri);
+          k = (MODE == 1) ? t : (adl0 ? t : ri);
+        }
+        acc[j][0] = fma(k, p2w.y, acc[j][0]);
+        acc[j][1] = fma(k, w12.x, acc[j][1]);
+        acc[j][2] = fma(k, w12.y, acc[j][2]);
+      }
+    }
+    int slots[4][3];
+    bool emit[4];
+    int tris[4];
+    bool any_emit = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double* cg = pr + j * REC + 6 * NQ;
+      const bool valid = 4 * p + j < ne;
+      const bool reg = row4::regular(sumsq_unfused(sub_rn(X0, mk3(cg[0], cg[1], cg[2]))), cg);
+      if (!reg) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
+      const int* meta = reinterpret_cast<const int*>(cg + 6);
+      const unsigned sl = static_cast<unsigned>(meta[2]), sf = static_cast<unsigned>(meta[3]);
+      slots[j][0] = valid ? (int)(sl & 0xffffu) : WIN;
+      slots[j][1] = valid ? (int)(sl >> 16) : WIN;
+      slots[j][2] = valid ? (int)(sf & 0xffffu) : WIN;
+      const bool prim = valid && (sf >> 16) & 1u;
+      tris[j] = valid ? meta[0] : 0;
+      emit[j] = !reg && prim && live0;
+      any_emit |= emit[j];
+    }
+    // deferred near pairs (rare): emitted from the panel's primary tile only
+    if (__any_sync(0xffffffffu, any_emit)) {
+      unsigned msk[4];
+      int total = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int* tc = a.tri_cols + 3 * (size_t)tris[j];
+        emit[j] = emit[j] && !(tc[0] == own0 || tc[1] == own0 || tc[2] == own0);
+        msk[j] = __ballot_sync(0xffffffffu, emit[j]);
+        total += __popc(msk[j]);
+      }
+      unsigned long long b = 0;
+      if (lane == 0 && total) b = atomicAdd(a.near_count, (unsigned long long)total);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      const unsigned lt = (1u << lane) - 1u;
+      long long off = (long long)b;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (emit[j]) {
+          const long long slot = off + __popc(msk[j] & lt);
+          if (slot < a.near_cap) {
+            a.near_list[2 * slot] = a.row_begin + i0;
+            a.near_list[2 * slot + 1] = tris[j];
+          }
+        }
+        off += __popc(msk[j]);
+      }
+    }
+    // window adds in record order (each lane owns its row: no conflicts)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      win[slots[j][0] * STRIDE + lane] += acc[j][0];
+      win[slots[j][1] * STRIDE + lane] += acc[j][1];
+      win[slots[j][2] * STRIDE + lane] += acc[j][2];
+    }
+    __syncwarp();
+  }
+  wait_group<0>();
+  __syncwarp();
+  while (base < width) {
+    flush32(base);
+    base += 32;
+  }
+}
+
+template <int WIN>
+static size_t row4_smem_bytes(int nq) {
+  return (size_t)(row4::Shape<WIN>::WREG + row4::DEPTH * 4 * (6 * nq + 8)) * sizeof(double);
+}
+
+template <int NQ, int WIN>
+static cudaError_t launch_row4_nq(const RegularArgs& a, int mode, cudaStream_t st) {
+  dim3 grid((a.n_rows + row4::ROWS - 1) / row4::ROWS, a.n_tiles);
+  const size_t smem = row4_smem_bytes<WIN>(NQ);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 32, smem, st>>>(a);
+    return cudaGetLastError();
+  };
+  if (mode == 0) return go(k_assemble_row4<NQ, 0, WIN>);
+  if (mode == 1) return go(k_assemble_row4<NQ, 1, WIN>);
+  return go(k_assemble_row4<NQ, 2, WIN>);
+}
+
+// window 64 (group-of-4 band <= 32) or 96 (<= 64)
+cudaError_t launch_regular_row4(const RegularArgs& a, int nq, int mode, int window, cudaStream_t st) {
+  auto pick = [&](auto win_tag) -> cudaError_t {
+    constexpr int W = decltype(win_tag)::value;
+    switch (nq) {
+      case 3: return launch_row4_nq<3, W>(a, mode, st);
+      case 6: return launch_row4_nq<6, W>(a, mode, st);
+      case 12: return launch_row4_nq<12, W>(a, mode, st);
+      case 16: return launch_row4_nq<16, W>(a, mode, st);
+    }
+    return cudaErrorInvalidValue;
+  };
+  if (window == 64) return pick(std::integral_constant<int, 64>{});
+  if (window == 96) return pick(std::integral_constant<int, 96>{});
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hvb

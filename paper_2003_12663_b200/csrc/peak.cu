@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(256) k_node_probe(double* out, int iters) {
       } else if (VAR == 1) {
         k0 = r20;
         k1 = r21;
+      } else if (VAR == 3) {
+        k0 = rsqrt2_newton(r20);
+        k1 = rsqrt2_newton(r21);
       } else {
         double y;
         asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r20));
@@ -149,6 +152,7 @@ extern "C" int hvb_bench_nodes(double* out, int var, int blocks, int threads, in
   cudaStream_t st = (cudaStream_t)stream;
   if (var == 0) hvb::k_node_probe<0><<<blocks, threads, 0, st>>>(out, iters);
   else if (var == 1) hvb::k_node_probe<1><<<blocks, threads, 0, st>>>(out, iters);
+  else if (var == 3) hvb::k_node_probe<3><<<blocks, threads, 0, st>>>(out, iters);
   else hvb::k_node_probe<2><<<blocks, threads, 0, st>>>(out, iters);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }

@@ -33,6 +33,14 @@ WINDOW_BAND = 64  # csrc/assemble_dual.cu: WIN - 32 for the default 96-column wi
 # for A/B measurements (tools/ab.sh)
 WINDOW = int(__import__("os").environ.get("HVB_ASM_WIN", "64"))
 STRIPS = __import__("os").environ.get("HVB_ASM_STRIPS", "1") == "1"
+# quad layout (csrc/assemble_quad.cu: 2 records x 2 rows per lane) needs the
+# band bounded over groups of 4 records; the dual layout over groups of 2
+# row4 layout (csrc/assemble_row4.cu: lane = row, 4 records per lane) uses
+# the same stream as quad
+LAYOUT = __import__("os").environ.get("HVB_ASM_LAYOUT", "row4")
+QUAD = LAYOUT in ("quad", "row4")
+GROUP = 4 if QUAD else 2
+LAYOUT_BITS = {"dual": 0, "quad": 8, "row4": 16}[LAYOUT]
 MAX_TILE = int(__import__("os").environ.get("HVB_ASM_MAXTILE", "32767"))
 
 
@@ -222,7 +230,8 @@ class DeviceMesh:
 
         # column tiling + panel streams
         self.window = WINDOW
-        tiling = mesh_tiling(mesh, max_tile, WINDOW, STRIPS)
+        tiling = mesh_tiling(mesh, max_tile, WINDOW, STRIPS, GROUP)
+        self.layout_bits = LAYOUT_BITS
         self.tiling = tiling
         self.perm = torch.as_tensor(tiling.perm, **i32)
         self.col_dev = torch.as_tensor(tiling.inv, **i32)
@@ -242,14 +251,14 @@ class DeviceMesh:
         self.n_tiles = len(tiling.tile_width)
 
 
-def mesh_tiling(mesh, max_tile: int = 2048, window: int = 96, strips: bool = False) -> ColumnTiling:
+def mesh_tiling(mesh, max_tile: int = 2048, window: int = 96, strips: bool = False, group: int = 2) -> ColumnTiling:
     """Host column tiling of a mesh (a mesh-derived array, cached on it)."""
-    key = ("tiling", max_tile, window, strips)
+    key = ("tiling", max_tile, window, strips, group)
     cache = mesh._device_cache
     t = cache.get(key)
     if t is None:
         t = column_tiling(mesh.colloc_points, mesh.tri_corner_cols, max_tile=max_tile, band_max=window - 32,
-                          strips=strips)
+                          group=group, strips=strips)
         cache[key] = t
     return t
 

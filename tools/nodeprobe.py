@@ -7,7 +7,7 @@ from paper_2003_12663_b200 import _lib
 out = torch.zeros(8, dtype=torch.float64, device="cuda")
 st = _lib.stream_ptr()
 iters = 2000
-for var, name, ops in ((0, "cubic", 14), (2, "quadratic", 13), (1, "no-rsqrt", 9)):
+for var, name, ops in ((0, "cubic", 14), (2, "quadratic", 13), (3, "rsqrt2", 12), (1, "no-rsqrt", 9)):
     for warps_per_sm in (4, 8, 12, 16, 32):
         threads = 128
         blocks = 148 * warps_per_sm // 4
