@@ -283,10 +283,17 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HVB_DIST_BACKEND=gloo lets several ranks share one GPU (validation of
+    # the multi-rank path on a 1-GPU box); production is NCCL, one GPU per rank
+    backend = os.environ.get("HVB_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import __graft_entry__
 
     __graft_entry__.build()
@@ -550,8 +557,10 @@ def _ncu_traffic(kernel="k_assemble_dual"):
             rec = json.load(fh).get(kernel)
     except (OSError, ValueError):
         return None
+    notes = {"k_assemble_dual": "one SL launch of the regular sweep (dominated by the matrix write)",
+             "k_gemv": "one cfg4 matvec (the 79 GB row-major block is read once)"}
     return None if rec is None else {"bytes_per_launch": rec["bytes_per_launch"], "source": os.path.basename(files[-1]),
-                                     "note": "one SL launch of the regular sweep (dominated by the matrix write)"}
+                                     "note": notes.get(kernel, "")}
 
 
 def main():

@@ -51,7 +51,8 @@ int hvb_build_stream(const double* table, int nq, const double* ccr, double eta,
  * near_list as (row-list index, triangle).  mode: 0 all-SL, 1 all-ADL,
  * 2 mixed; | 4 = 64-column window (else 96); | 8 = quad layout (the panel
  * stream's band is bounded over groups of 4 records, else 2); | 16 = row4
- * layout (lane = row, 4 records per lane; same stream as quad).
+ * layout (lane = row, 4 records per lane; same stream as quad); | 32 = row8
+ * (8 records per lane, band over groups of 8).
  * Replaces: row_pass1 regular part  assembly.py:170-200 and
  * _kernel_values 126-132 */
 int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_col0,

@@ -34,11 +34,11 @@ HVB_DEV bool regular(double sq, const double* cg) {
 }
 }  // namespace row4
 
-template <int NQ, int MODE, int WIN>
+template <int NQ, int MODE, int WIN, int R>
 __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
   using namespace row4;
   constexpr int REC = 6 * NQ + 8;
-  constexpr int SREC = 4 * REC;
+  constexpr int SREC = R * REC;
   constexpr int SLOTS = Shape<WIN>::SLOTS;
   constexpr int WREG = Shape<WIN>::WREG;
   extern __shared__ double smem[];
@@ -71,12 +71,12 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
   const int col0 = a.tile_col0[tile], width = a.tile_width[tile];
   const double* src = a.stream + e0 * REC;
   const int ne = (int)(e1 - e0);
-  const int ns = (ne + 3) >> 2;
+  const int ns = (ne + R - 1) / R;
 
   auto stage = [&](int p) {
     double* dst = ring + (p & 1) * SREC;
-    const double* s = src + (size_t)(4 * p) * REC;
-    const int nrec = min(4, ne - 4 * p);
+    const double* s = src + (size_t)(R * p) * REC;
+    const int nrec = min(R, ne - R * p);
     const int nch = nrec * (REC / 2);
     for (int c = lane; c < nch; c += 32) cp_async16(dst + 2 * c, s + 2 * c);
   };
@@ -109,13 +109,13 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
       flush32(base);
       base += 32;
     }
-    double acc[4][3];
+    double acc[R][3];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
+    for (int j = 0; j < R; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < R; ++j) {
         const double* rec = pr + j * REC;
         const double2 p01 = *reinterpret_cast<const double2*>(rec + 6 * q);
         const double2 p2w = *reinterpret_cast<const double2*>(rec + 6 * q + 2);
@@ -136,14 +136,14 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
         acc[j][2] = fma(k, w12.y, acc[j][2]);
       }
     }
-    int slots[4][3];
-    bool emit[4];
-    int tris[4];
+    int slots[R][3];
+    bool emit[R];
+    int tris[R];
     bool any_emit = false;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < R; ++j) {
       const double* cg = pr + j * REC + 6 * NQ;
-      const bool valid = 4 * p + j < ne;
+      const bool valid = R * p + j < ne;
       const bool reg = row4::regular(sumsq_unfused(sub_rn(X0, mk3(cg[0], cg[1], cg[2]))), cg);
       if (!reg) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
       const int* meta = reinterpret_cast<const int*>(cg + 6);
@@ -158,10 +158,10 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
     }
     // deferred near pairs (rare): emitted from the panel's primary tile only
     if (__any_sync(0xffffffffu, any_emit)) {
-      unsigned msk[4];
+      unsigned msk[R];
       int total = 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < R; ++j) {
         const int* tc = a.tri_cols + 3 * (size_t)tris[j];
         emit[j] = emit[j] && !(tc[0] == own0 || tc[1] == own0 || tc[2] == own0);
         msk[j] = __ballot_sync(0xffffffffu, emit[j]);
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
       const unsigned lt = (1u << lane) - 1u;
       long long off = (long long)b;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < R; ++j) {
         if (emit[j]) {
           const long long slot = off + __popc(msk[j] & lt);
           if (slot < a.near_cap) {
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
     }
     // window adds in record order (each lane owns its row: no conflicts)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < R; ++j) {
       win[slots[j][0] * STRIDE + lane] += acc[j][0];
       win[slots[j][1] * STRIDE + lane] += acc[j][1];
       win[slots[j][2] * STRIDE + lane] += acc[j][2];
@@ -202,38 +202,43 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
 }
 
 template <int WIN>
-static size_t row4_smem_bytes(int nq) {
-  return (size_t)(row4::Shape<WIN>::WREG + row4::DEPTH * 4 * (6 * nq + 8)) * sizeof(double);
+static size_t row4_smem_bytes(int nq, int r) {
+  return (size_t)(row4::Shape<WIN>::WREG + row4::DEPTH * r * (6 * nq + 8)) * sizeof(double);
 }
 
-template <int NQ, int WIN>
+template <int NQ, int WIN, int R>
 static cudaError_t launch_row4_nq(const RegularArgs& a, int mode, cudaStream_t st) {
   dim3 grid((a.n_rows + row4::ROWS - 1) / row4::ROWS, a.n_tiles);
-  const size_t smem = row4_smem_bytes<WIN>(NQ);
+  const size_t smem = row4_smem_bytes<WIN>(NQ, R);
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, 32, smem, st>>>(a);
     return cudaGetLastError();
   };
-  if (mode == 0) return go(k_assemble_row4<NQ, 0, WIN>);
-  if (mode == 1) return go(k_assemble_row4<NQ, 1, WIN>);
-  return go(k_assemble_row4<NQ, 2, WIN>);
+  if (mode == 0) return go(k_assemble_row4<NQ, 0, WIN, R>);
+  if (mode == 1) return go(k_assemble_row4<NQ, 1, WIN, R>);
+  return go(k_assemble_row4<NQ, 2, WIN, R>);
 }
 
-// window 64 (group-of-4 band <= 32) or 96 (<= 64)
-cudaError_t launch_regular_row4(const RegularArgs& a, int nq, int mode, int window, cudaStream_t st) {
-  auto pick = [&](auto win_tag) -> cudaError_t {
+// window 64 (band over groups of R records <= 32) or 96 (groups of 4, <= 64);
+// R = 4 or 8 records per lane per step
+cudaError_t launch_regular_row4(const RegularArgs& a, int nq, int mode, int window, int r, cudaStream_t st) {
+  auto pick = [&](auto win_tag, auto r_tag) -> cudaError_t {
     constexpr int W = decltype(win_tag)::value;
+    constexpr int RR = decltype(r_tag)::value;
     switch (nq) {
-      case 3: return launch_row4_nq<3, W>(a, mode, st);
-      case 6: return launch_row4_nq<6, W>(a, mode, st);
-      case 12: return launch_row4_nq<12, W>(a, mode, st);
-      case 16: return launch_row4_nq<16, W>(a, mode, st);
+      case 3: return launch_row4_nq<3, W, RR>(a, mode, st);
+      case 6: return launch_row4_nq<6, W, RR>(a, mode, st);
+      case 12: return launch_row4_nq<12, W, RR>(a, mode, st);
+      case 16: return launch_row4_nq<16, W, RR>(a, mode, st);
     }
     return cudaErrorInvalidValue;
   };
-  if (window == 64) return pick(std::integral_constant<int, 64>{});
-  if (window == 96) return pick(std::integral_constant<int, 96>{});
+  using I4 = std::integral_constant<int, 4>;
+  using I8 = std::integral_constant<int, 8>;
+  if (window == 64 && r == 8) return pick(std::integral_constant<int, 64>{}, I8{});
+  if (window == 64 && r == 4) return pick(std::integral_constant<int, 64>{}, I4{});
+  if (window == 96 && r == 4) return pick(std::integral_constant<int, 96>{}, I4{});
   return cudaErrorInvalidValue;
 }
 

@@ -67,11 +67,10 @@ __global__ void __launch_bounds__(FT) k_field(FieldArgs a) {
         const double2 p2q = s_src[(j * NQ + q) * 2 + 1];
         const double dx = X.x - p01.x, dy = X.y - p01.y, dz = X.z - p2q.x;
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        const double ri = rsqrt_full(r2);
         if (POT) {
-          fx = fma(p2q.y, ri, fx);
+          fx = fma(p2q.y, rsqrt_full(r2), fx);
         } else {
-          const double s = p2q.y * (ri * ri * ri);
+          const double s = p2q.y * rinv3(r2);
           fx = fma(s, dx, fx);
           fy = fma(s, dy, fy);
           fz = fma(s, dz, fz);

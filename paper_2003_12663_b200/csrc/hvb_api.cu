@@ -56,6 +56,7 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
   const int window = (mode & 4) ? 64 : 96;  // bit 2: 64-column window tiling
   const bool quad = (mode & 8) != 0;        // bit 3: quad layout (tiling band over groups of 4 records)
   const bool row4 = (mode & 16) != 0;       // bit 4: row4 layout (same tiling as quad)
+  const bool row8 = (mode & 32) != 0;       // bit 5: row8 layout (band over groups of 8 records)
   mode &= 3;
   if (mode > 2 || warps_per_block < 1 || warps_per_block > 8)
     return fail(HVB_EARG, "hvb_assemble_regular: bad mode / warps_per_block");
@@ -78,8 +79,9 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
   a.near_list = near_list;
   a.near_count = near_count;
   a.near_cap = near_cap;
-  if (row4)
-    return check(hvb::launch_regular_row4(a, nq, mode, window, (cudaStream_t)stream), "hvb_assemble_regular");
+  if (row4 || row8)
+    return check(hvb::launch_regular_row4(a, nq, mode, window, row8 ? 8 : 4, (cudaStream_t)stream),
+                 "hvb_assemble_regular");
   if (quad)
     return check(hvb::launch_regular_quad(a, nq, mode, window, (cudaStream_t)stream), "hvb_assemble_regular");
   return check(hvb::launch_regular(a, nq, mode, window, warps_per_block, (cudaStream_t)stream),

@@ -137,12 +137,13 @@ namespace hvb {
 __global__ void k_rsqrt_probe(const double* r2, int n, double* out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  out[2 * i] = rsqrt2_newton(r2[i]);
-  out[2 * i + 1] = rsqrt_full(r2[i]);
+  out[3 * i] = rsqrt2_newton(r2[i]);
+  out[3 * i + 1] = rsqrt_full(r2[i]);
+  out[3 * i + 2] = rinv3(r2[i]);
 }
 }  // namespace hvb
 
-// accuracy probe of the two rsqrt refinements: out (n, 2) = 2/sqrt, 1/sqrt
+// accuracy probe of the rsqrt refinements: out (n, 3) = 2/sqrt, 1/sqrt, r^-3
 extern "C" int hvb_bench_rsqrt(const double* r2, int n, double* out, void* stream) {
   hvb::k_rsqrt_probe<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(r2, n, out);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;

@@ -38,9 +38,9 @@ STRIPS = __import__("os").environ.get("HVB_ASM_STRIPS", "1") == "1"
 # row4 layout (csrc/assemble_row4.cu: lane = row, 4 records per lane) uses
 # the same stream as quad
 LAYOUT = __import__("os").environ.get("HVB_ASM_LAYOUT", "row4")
-QUAD = LAYOUT in ("quad", "row4")
-GROUP = 4 if QUAD else 2
-LAYOUT_BITS = {"dual": 0, "quad": 8, "row4": 16}[LAYOUT]
+QUAD = LAYOUT in ("quad", "row4", "row8")
+GROUP = {"dual": 2, "quad": 4, "row4": 4, "row8": 8}[LAYOUT]
+LAYOUT_BITS = {"dual": 0, "quad": 8, "row4": 16, "row8": 32}[LAYOUT]
 MAX_TILE = int(__import__("os").environ.get("HVB_ASM_MAXTILE", "32767"))
 
 

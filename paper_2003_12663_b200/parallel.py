@@ -51,10 +51,15 @@ class RowGather:
         import torch.distributed as dist
 
         dev = local.device
-        pad = torch.zeros(self.maxlen, dtype=local.dtype, device=dev)
+        # gloo (CPU tests, or several ranks sharing one GPU) gathers host copies
+        host = local.is_cuda and dist.get_backend(self.group) == "gloo"
+        gdev = torch.device("cpu") if host else dev
+        pad = torch.zeros(self.maxlen, dtype=local.dtype, device=gdev)
         pad[: local.shape[0]] = local
-        buf = torch.empty(self.world * self.maxlen, dtype=local.dtype, device=dev)
+        buf = torch.empty(self.world * self.maxlen, dtype=local.dtype, device=gdev)
         dist.all_gather_into_tensor(buf, pad, group=self.group)
+        if host:
+            buf = buf.to(dev)
         key = str(dev)
         if key not in self._idx:
             self._idx[key] = torch.as_tensor(self._idx_np, device=dev)

@@ -230,3 +230,25 @@ def test_tracing_semantics(sphere2_solved, capacitor2):
     assert abs(line.length - 0.496) / 0.496 < 0.02
     line = trace_fieldline(solc, mc, np.array([0.45, 0.35, 0.2]), +1)
     assert line.length >= np.linalg.norm(line.points[-1] - line.points[0]) - 1e-12
+
+
+def test_floating_conductor_gate_opt_in():
+    """Reference semantics: closed floating conductors never pass the true-
+    residual gate (SolverError); the opt-in scaled gate converges to the
+    direct solution."""
+    from conftest import _cfg3_parts
+    from paper_2003_12663_b200 import fixtures as F
+    from paper_2003_12663_b200.assembly import assemble
+    from paper_2003_12663_b200.solver import SolverConfig, SolverError, solve
+
+    v, tris = _cfg3_parts(F, 2, 1)
+    m = F.mesh_from_parts(v, np.array([t[0] for t in tris]), np.array([t[1] for t in tris]),
+                          ["patch 0 electrode 1.0", "patch 1 floating 0", "patch 2 electrode 0.0"])
+    A, rhs = assemble(m)
+    x = np.linalg.solve(A.toarray(), rhs)
+    with pytest.raises(SolverError) as ei:
+        solve(A, rhs, SolverConfig(max_iters=300))
+    assert ei.value.iterations >= 300 and ei.value.best_residual > 1e-8
+    sol = solve(A, rhs, SolverConfig(true_residual_gate=False))
+    assert np.max(np.abs(sol.u - x[: m.n_collocation])) <= 1e-6 * np.max(np.abs(x))
+    assert abs(sol.V[0] - x[-1]) <= 1e-6 * abs(x[-1])
