@@ -135,7 +135,8 @@ int hvb_field_singular(const double* nodes6, const int* tri_cols, const int* vc_
  * start; mode 1 consumes E results (e_out/e_flag, indexed by the previous
  * request slots); mode 2 consumes surface distances (sd_out).  New E / SD
  * requests are appended to e_pts/e_line and sd_pts/sd_line through
- * counters[0] / counters[1]; counters[2] = max points per line; polylines (n_lines, cap, 5) = x, y, z, |E|, s.
+ * counters[0] / counters[1]; counters[2] = max points per line, counters[3] =
+ * total E requests; polylines (n_lines, cap, 5) = x, y, z, |E|, s.
  * Replaces: trace_fieldline  postprocess.py:244-357 (control flow, step
  * control, surface-hit snapping, termination order) */
 int hvb_line_state_bytes(void);
@@ -143,6 +144,25 @@ int hvb_trace_ctrl(void* state, int n_lines, const double* starts, const int* or
                    double* e_pts, int* e_line, double* sd_pts, int* sd_line, unsigned long long* counters,
                    const double* e_out, const int* e_flag, const double* sd_out, double* out_pts,
                    int cap, void* stream);
+
+/* One tracer round with no host synchronisation: the field of the current
+ * request list cur_pts (count = counters[0], on the device; N-body over
+ * src/cls with `split` panel chunks into part (split, n_lines, 4); has_near
+ * (split, n_lines) int32 chunk flags, zero on entry and left zero; near pass
+ * per flagged chunk in panel order with vertex-coincidence flags), then
+ * counters[0..1] = 0, the consume-E control step (new requests into
+ * nxt_pts/nxt_line), the surface distances of counters[1] queries and the
+ * consume-SD control step.  Rounds are enqueued back to back; the host
+ * reads counters only every few rounds.  Replaces: the per-stage
+ * eval_efield / _surface_distance calls of trace_fieldline
+ * postprocess.py:262-330 */
+int hvb_trace_round(void* state, int n_lines, const double* geo, double* cur_pts, double* nxt_pts, int* nxt_line,
+                    double* sd_pts, int* sd_line, double* sd_out, unsigned long long* counters, double* e_out,
+                    int* e_flag, int* has_near, double* part, const double* src, const double* cls,
+                    const int* tri_cols, int nt, int nq, int split, const double* nodes6, const double* radii,
+                    const double* ccr, const double* u, const double* duffy, int n_duffy, const double* graded,
+                    int n_graded, int bisect_depth, double bisect_trigger, double prox, double* out_pts, int cap,
+                    void* stream);
 
 /* per line (npts, termination, status, phase) and the start |E| of a
  * weak-start line */

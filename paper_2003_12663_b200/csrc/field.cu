@@ -34,21 +34,22 @@ __global__ void k_contract(const double* __restrict__ table, int nt, int nq, con
 constexpr int FT = 128;   // targets per CTA
 constexpr int FCH = 32;   // panels per shared-memory chunk
 
+// One (target block bx, panel split by) tile of the N-body sum.  Called by
+// every thread of the CTA (it synchronises).  near_list == nullptr: instead
+// of emitting (target, panel) near pairs, set has_near[target] = 1.
 template <int NQ, int POT>
-__global__ void __launch_bounds__(FT) k_field(FieldArgs a) {
-  __shared__ double2 s_src[FCH * NQ * 2];
-  __shared__ double s_cls[FCH * 6];
-  __shared__ int s_cols[FCH * 3];
+HVB_DEV void field_tile(const FieldArgs& a, int bx, int by, double2* s_src, double* s_cls, int* s_cols) {
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int ti = blockIdx.x * FT + tid;
+  const int ti = bx * FT + tid;
   const bool live = ti < a.m;
   const int tt = live ? ti : a.m - 1;
   const d3 X = mk3(a.pts[3 * (size_t)tt], a.pts[3 * (size_t)tt + 1], a.pts[3 * (size_t)tt + 2]);
   const int own = a.own_col ? a.own_col[tt] : -1;
-  const int tb = (int)((long long)a.nt * blockIdx.y / a.split);
-  const int te = (int)((long long)a.nt * (blockIdx.y + 1) / a.split);
+  const int tb = (int)((long long)a.nt * by / a.split);
+  const int te = (int)((long long)a.nt * (by + 1) / a.split);
   double ex = 0.0, ey = 0.0, ez = 0.0;
+  bool any_near = false;
   for (int c0 = tb; c0 < te; c0 += FCH) {
     const int cn = min(FCH, te - c0);
     __syncthreads();
@@ -86,6 +87,10 @@ __global__ void __launch_bounds__(FT) k_field(FieldArgs a) {
         const int* tc = s_cols + 3 * j;
         emit = !(own >= 0 && (tc[0] == own || tc[1] == own || tc[2] == own));
       }
+      if (a.near_list == nullptr) {
+        any_near |= emit;
+        continue;
+      }
       const unsigned msk = __ballot_sync(0xffffffffu, emit);
       if (msk) {
         unsigned long long b = 0;
@@ -102,11 +107,53 @@ __global__ void __launch_bounds__(FT) k_field(FieldArgs a) {
     }
   }
   if (live) {
-    double* o = a.part + ((size_t)blockIdx.y * a.m + ti) * 4;
+    double* o = a.part + ((size_t)by * a.m + ti) * 4;
     o[0] = ex;
     o[1] = ey;
     o[2] = ez;
     o[3] = 0.0;
+    if (any_near) a.has_near[(size_t)by * a.m + ti] = 1;  // (split, m) chunk flags
+  }
+}
+
+template <int NQ, int POT>
+__global__ void __launch_bounds__(FT) k_field(FieldArgs a) {
+  __shared__ double2 s_src[FCH * NQ * 2];
+  __shared__ double s_cls[FCH * 6];
+  __shared__ int s_cols[FCH * 3];
+  field_tile<NQ, POT>(a, blockIdx.x, blockIdx.y, s_src, s_cls, s_cols);
+}
+
+// Same tiles, target count read on the device (*m_dev) and a grid-stride
+// loop over (target block, split) items: launchable without knowing the
+// count on the host (the tracer's sync-free rounds).  part is (split, m, 4)
+// with the row stride of the CURRENT count.
+template <int NQ>
+__global__ void __launch_bounds__(FT) k_field_dyn(FieldArgs a, const unsigned long long* m_dev) {
+  __shared__ double2 s_src[FCH * NQ * 2];
+  __shared__ double s_cls[FCH * 6];
+  __shared__ int s_cols[FCH * 3];
+  a.m = (int)*m_dev;
+  const int nb = (a.m + FT - 1) / FT;
+  const long long items = (long long)nb * a.split;
+  for (long long it = blockIdx.x; it < items; it += gridDim.x)
+    field_tile<NQ, 0>(a, (int)(it % nb), (int)(it / nb), s_src, s_cls, s_cols);
+}
+
+// fixed-order reduction of the panel splits, count on the device
+__global__ void k_field_reduce_dyn(const double* part, int split, const unsigned long long* m_dev, double* out) {
+  const int m = (int)*m_dev;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    double s0 = 0, s1 = 0, s2 = 0;
+    for (int s = 0; s < split; ++s) {
+      const double* p = part + ((size_t)s * m + i) * 4;
+      s0 += p[0];
+      s1 += p[1];
+      s2 += p[2];
+    }
+    out[3 * (size_t)i] = s0;
+    out[3 * (size_t)i + 1] = s1;
+    out[3 * (size_t)i + 2] = s2;
   }
 }
 
@@ -137,10 +184,13 @@ __global__ void k_near_apply_points(const int* seg_ptr, int n_seg, const int* pa
     const int* tc = tri_cols + 3 * (size_t)t;
     const double* c = contrib + 9 * (size_t)p;
     double* o = out + 3 * (size_t)i;
+    const double u0 = u[tc[0]], u1 = u[tc[1]], u2 = u[tc[2]];
     if (potential) {
-      o[0] += u[tc[0]] * c[0] + u[tc[1]] * c[1] + u[tc[2]] * c[2];
+      o[0] = __dadd_rn(o[0], __fma_rn(u2, c[2], __fma_rn(u1, c[1], __dmul_rn(u0, c[0]))));
     } else {
-      for (int d = 0; d < 3; ++d) o[d] += u[tc[0]] * c[d] + u[tc[1]] * c[3 + d] + u[tc[2]] * c[6 + d];
+      // same operation order as the tracer's near pass (trace.cu k_trace_near)
+      for (int d = 0; d < 3; ++d)
+        o[d] = __dadd_rn(o[d], __fma_rn(u2, c[6 + d], __fma_rn(u1, c[3 + d], __dmul_rn(u0, c[d]))));
     }
   }
 }
@@ -222,6 +272,19 @@ cudaError_t launch_contract(const double* table, int nt, int nq, const int* tri_
                             cudaStream_t st) {
   int n = nt * nq;
   k_contract<<<(n + 255) / 256, 256, 0, st>>>(table, nt, nq, tri_cols, u, src);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_field_dyn(const FieldArgs& a, const unsigned long long* m_dev, int grid, cudaStream_t st) {
+  switch (a.nq) {
+    case 3: k_field_dyn<3><<<grid, FT, 0, st>>>(a, m_dev); break;
+    case 6: k_field_dyn<6><<<grid, FT, 0, st>>>(a, m_dev); break;
+    case 12: k_field_dyn<12><<<grid, FT, 0, st>>>(a, m_dev); break;
+    case 16: k_field_dyn<16><<<grid, FT, 0, st>>>(a, m_dev); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (cudaGetLastError() != cudaSuccess) return cudaErrorLaunchFailure;
+  k_field_reduce_dyn<<<1184, 128, 0, st>>>(a.part, a.split, m_dev, a.out);
   return cudaGetLastError();
 }
 

@@ -190,6 +190,8 @@ int hvb_field(const double* src, const double* cls, const int* tri_cols, int nt,
   a.near_list = near_list;
   a.near_count = near_count;
   a.near_cap = near_cap;
+  a.has_near = nullptr;
+  a.out = nullptr;
   return check(hvb::launch_field(a, (cudaStream_t)stream), "hvb_field");
 }
 
@@ -248,6 +250,72 @@ int hvb_trace_ctrl(void* state, int n_lines, const double* starts, const int* or
   a.out_pts = out_pts;
   a.cap = cap;
   return check(hvb::launch_trace_ctrl(a, mode, (cudaStream_t)stream), "hvb_trace_ctrl");
+}
+
+int hvb_trace_round(void* state, int n_lines, const double* geo, double* cur_pts, double* nxt_pts, int* nxt_line,
+                    double* sd_pts, int* sd_line, double* sd_out, unsigned long long* counters, double* e_out,
+                    int* e_flag, int* has_near, double* part, const double* src, const double* cls,
+                    const int* tri_cols, int nt, int nq, int split, const double* nodes6, const double* radii,
+                    const double* ccr, const double* u, const double* duffy, int n_duffy, const double* graded,
+                    int n_graded, int bisect_depth, double bisect_trigger, double prox, double* out_pts, int cap,
+                    void* stream) {
+  if (n_lines < 0 || cap < 2 || split < 1) return fail(HVB_EARG, "hvb_trace_round: bad n_lines/cap/split");
+  hvb::TraceRoundArgs r;
+  hvb::TraceArgs& a = r.ctrl;
+  a.state = static_cast<hvb::LineState*>(state);
+  a.n_lines = n_lines;
+  a.starts = nullptr;
+  a.orient = nullptr;
+  for (int d = 0; d < 3; ++d) {
+    a.center[d] = geo[d];
+    a.half[d] = geo[3 + d];
+  }
+  a.diag = geo[6];
+  a.h_min = geo[7];
+  a.h_max = geo[8];
+  a.l_max = geo[9];
+  a.rel_tol = geo[10];
+  a.tol_frac = geo[11];
+  a.e_floor = geo[12];
+  a.e_pts = nxt_pts;
+  a.e_line = nxt_line;
+  a.sd_pts = sd_pts;
+  a.sd_line = sd_line;
+  a.counters = counters;
+  a.e_out = e_out;
+  a.e_flag = e_flag;
+  a.sd_out = sd_out;
+  a.out_pts = out_pts;
+  a.cap = cap;
+  hvb::FieldArgs& f = r.field;
+  f.src = src;
+  f.cls = cls;
+  f.tri_cols = tri_cols;
+  f.nt = nt;
+  f.nq = nq;
+  f.pts = cur_pts;
+  f.own_col = nullptr;
+  f.m = 0;
+  f.split = split;
+  f.potential = 0;
+  f.part = part;
+  f.near_list = nullptr;
+  f.near_count = nullptr;
+  f.near_cap = 0;
+  f.has_near = has_near;
+  f.out = e_out;
+  r.nodes6 = nodes6;
+  r.radii = radii;
+  r.ccr = ccr;
+  r.u = u;
+  r.duffy = duffy;
+  r.n_duffy = n_duffy;
+  r.graded = graded;
+  r.n_graded = n_graded;
+  r.bisect_depth = bisect_depth;
+  r.bisect_trigger = bisect_trigger;
+  r.prox = prox;
+  return check(hvb::launch_trace_round(r, (cudaStream_t)stream), "hvb_trace_round");
 }
 
 int hvb_trace_summary(const void* state, int n_lines, int* info, double* dinfo, void* stream) {

@@ -74,9 +74,11 @@ struct FieldArgs {
   int split;              // panel-range split (grid.y)
   int potential;          // 1: phi, 0: E
   double* part;           // (split, m, 4) partial sums
-  int* near_list;         // (cap, 2): (target, triangle)
+  int* near_list;         // (cap, 2): (target, triangle); nullptr: set has_near instead
   unsigned long long* near_count;
   long long near_cap;
+  int* has_near;          // (split, m) chunk flags (dynamic / tracer path)
+  double* out;            // (m, 3) reduced field (dynamic path)
 };
 
 cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, int window, int wpb, cudaStream_t st);
@@ -100,6 +102,7 @@ cudaError_t launch_gather_scale(const double* z, const double* right, const int*
 cudaError_t launch_rowmax_diag(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const int* diag_col,
                                double* rowmax, double* diag, cudaStream_t st);
 cudaError_t launch_field(const FieldArgs& a, cudaStream_t st);
+cudaError_t launch_field_dyn(const FieldArgs& a, const unsigned long long* m_dev, int grid, cudaStream_t st);
 cudaError_t launch_contract(const double* table, int nt, int nq, const int* tri_cols, const double* u, double* src,
                             cudaStream_t st);
 cudaError_t launch_field_reduce(const double* part, int split, int m, double* out, cudaStream_t st);
@@ -137,7 +140,8 @@ struct TraceArgs {
   int* e_line;
   double* sd_pts;         // (n_lines, 3)
   int* sd_line;
-  unsigned long long* counters;  // [0] E requests, [1] SD requests, [2] max points per line
+  unsigned long long* counters;  // [0] E requests, [1] SD requests, [2] max points per line,
+                                 // [3] total E requests (never reset)
   // results of the previous requests
   const double* e_out;    // (n_req, 3)
   const int* e_flag;      // (n_req) 1 = coincident with a mesh vertex
@@ -147,7 +151,27 @@ struct TraceArgs {
   int cap;
 };
 
+// one sync-free tracer round (trace.cu): field.pts = current request list,
+// field.out = ctrl.e_out, field.has_near = scratch flags; ctrl.e_pts/e_line =
+// the next request list
+struct TraceRoundArgs {
+  TraceArgs ctrl;
+  FieldArgs field;
+  const double* nodes6;
+  const double* radii;
+  const double* ccr;
+  const double* u;
+  const double* duffy;
+  int n_duffy;
+  const double* graded;
+  int n_graded;
+  int bisect_depth;
+  double bisect_trigger;
+  double prox;
+};
+
 cudaError_t launch_trace_ctrl(const TraceArgs& a, int mode, cudaStream_t st);
+cudaError_t launch_trace_round(const TraceRoundArgs& r, cudaStream_t st);
 cudaError_t launch_surface_distance(const double* pts, int m, const double* ccr, int nt, const double* nodes6,
                                     double* out, cudaStream_t st);
 cudaError_t launch_near_coincide(const int* pairs, long long n_pairs, const double* pts, const double* nodes6,

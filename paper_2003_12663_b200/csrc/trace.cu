@@ -26,7 +26,7 @@
 // stage-6 point itself (same coefficients), which lets the accepted point
 // reuse the stage-6 field instead of evaluating E(x5) a second time:
 // 6 field evaluations per accepted step instead of the reference's 7.
-#include "launch.cuh"
+#include "near.cuh"
 
 namespace hvb {
 
@@ -54,6 +54,7 @@ HVB_DEV void request_e(const TraceArgs& a, LineState& L, int line, const double*
   L.req[1] = p[1];
   L.req[2] = p[2];
   const unsigned long long slot = atomicAdd(&a.counters[0], 1ull);
+  atomicAdd(&a.counters[3], 1ull);  // field evaluations, never reset
   L.slot = (int)slot;
   a.e_pts[3 * slot] = p[0];
   a.e_pts[3 * slot + 1] = p[1];
@@ -309,7 +310,9 @@ HVB_DEV d3 map_reference_blas(const double* __restrict__ X, double u, double v) 
 constexpr int SD_THREADS = 256;
 constexpr int SD_K = 12;
 
-__global__ void __launch_bounds__(SD_THREADS) k_surface_distance(const double* __restrict__ pts, int m,
+// m_dev != nullptr: the query count is read on the device (tracer rounds)
+__global__ void __launch_bounds__(SD_THREADS) k_surface_distance(const double* __restrict__ pts, int m_host,
+                                                                 const unsigned long long* m_dev,
                                                                  const double* __restrict__ ccr, int nt,
                                                                  const double* __restrict__ nodes6,
                                                                  double* __restrict__ out) {
@@ -317,8 +320,9 @@ __global__ void __launch_bounds__(SD_THREADS) k_surface_distance(const double* _
   __shared__ int s_idx[SD_THREADS * SD_K];
   __shared__ double s_d[SD_K];
   __shared__ int s_t[SD_K];
-  const int q = blockIdx.x;
-  if (q >= m) return;
+  const int m = m_dev ? (int)*m_dev : m_host;
+  for (int q = blockIdx.x; q < m; q += gridDim.x) {
+  __syncthreads();
   const int tid = threadIdx.x;
   const d3 X = mk3(pts[3 * (size_t)q], pts[3 * (size_t)q + 1], pts[3 * (size_t)q + 2]);
   double key[SD_K];
@@ -403,6 +407,7 @@ __global__ void __launch_bounds__(SD_THREADS) k_surface_distance(const double* _
     out[2 * (size_t)q] = best;
     out[2 * (size_t)q + 1] = bt < nt ? ccr[4 * (size_t)bt + 3] : 0.0;
   }
+  }  // queries
 }
 
 // near-pair vertex coincidence: flag targets within `prox` of a node of a
@@ -469,6 +474,120 @@ cudaError_t launch_trace_summary(const LineState* state, int n_lines, int* info,
   return cudaGetLastError();
 }
 
+// Near pass of one tracer round, without a host-side pair list: the field
+// kernel flags each (panel chunk, target) holding a non-regular panel; one
+// warp per target rescans only the flagged chunks, in chunk then panel
+// order, clearing the flags as it goes.  Every non-regular panel gets the
+// vertex-coincidence check and its composite-rule field, added to the
+// target in panel order -- the same order and arithmetic as the sorted-pair
+// path (k_near_pairs + k_near_apply_points), so results are bitwise those
+// of eval_efield_batch.
+__global__ void k_trace_near(const unsigned long long* m_dev, int split, const double* __restrict__ pts,
+                             int* __restrict__ has_near, const double* __restrict__ cls,
+                             const double* __restrict__ nodes6, const double* __restrict__ radii,
+                             const int* __restrict__ tri_cols, int nt, const double* __restrict__ u,
+                             const double* duffy, int n_duffy, const double* graded, int n_graded, int bisect_depth,
+                             double bisect_trigger, double prox, double* __restrict__ E, int* __restrict__ flag) {
+  const int lane = threadIdx.x & 31;
+  const int m = (int)*m_dev;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m; i += warps) {
+    const d3 X = mk3(pts[3 * (size_t)i], pts[3 * (size_t)i + 1], pts[3 * (size_t)i + 2]);
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0;
+    bool any = false, coinc = false;
+    for (int cb = 0; cb < split; cb += 32) {
+      const int cc = cb + lane;
+      int* fp = has_near + (size_t)cc * m + i;
+      const bool fl = cc < split && *fp;
+      if (fl) *fp = 0;
+      unsigned cm = __ballot_sync(0xffffffffu, fl);
+      while (cm) {
+        const int chunk = cb + __ffs(cm) - 1;
+        cm &= cm - 1;
+        if (!any) {
+          any = true;
+          e0 = E[3 * (size_t)i];
+          e1 = E[3 * (size_t)i + 1];
+          e2 = E[3 * (size_t)i + 2];
+        }
+        const int tb = (int)((long long)nt * chunk / split);
+        const int te = (int)((long long)nt * (chunk + 1) / split);
+        for (int t0 = tb; t0 < te; t0 += 32) {
+          const int t = t0 + lane;
+          bool nr = false;
+          if (t < te) {
+            const double* c = cls + 6 * (size_t)t;
+            nr = !is_regular(X, mk3(c[0], c[1], c[2]), c[3], c[4], c[5]);
+          }
+          unsigned msk = __ballot_sync(0xffffffffu, nr);
+          while (msk) {
+            const int tn = t0 + __ffs(msk) - 1;
+            msk &= msk - 1;
+            const double* Xn = nodes6 + 18 * (size_t)tn;
+            if (lane < 6) {
+              const double d =
+                  __dsqrt_rn(sumsq_unfused(sub_rn(X, mk3(Xn[3 * lane], Xn[3 * lane + 1], Xn[3 * lane + 2]))));
+              if (d < prox) coinc = true;
+            }
+            double acc[9];
+            near_pair_acc(X, mk3(0.0, 0.0, 0.0), 2, Xn, radii[tn], duffy, n_duffy, graded, n_graded, bisect_depth,
+                          bisect_trigger, acc);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) acc[k] = warp_sum(acc[k]);
+            const int* tc = tri_cols + 3 * (size_t)tn;
+            const double u0 = u[tc[0]], u1 = u[tc[1]], u2 = u[tc[2]];
+            e0 = __dadd_rn(e0, __fma_rn(u2, acc[6], __fma_rn(u1, acc[3], __dmul_rn(u0, acc[0]))));
+            e1 = __dadd_rn(e1, __fma_rn(u2, acc[7], __fma_rn(u1, acc[4], __dmul_rn(u0, acc[1]))));
+            e2 = __dadd_rn(e2, __fma_rn(u2, acc[8], __fma_rn(u1, acc[5], __dmul_rn(u0, acc[2]))));
+          }
+        }
+      }
+    }
+    coinc = __any_sync(0xffffffffu, coinc);
+    if (lane == 0 && any) {
+      E[3 * (size_t)i] = e0;
+      E[3 * (size_t)i + 1] = e1;
+      E[3 * (size_t)i + 2] = e2;
+      if (coinc) flag[i] = 1;
+    }
+  }
+}
+
+__global__ void k_trace_reset_flags(int* flag, int n) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) flag[k] = 0;
+}
+
+__global__ void k_trace_reset_counters(unsigned long long* counters) {
+  if (threadIdx.x < 2) counters[threadIdx.x] = 0;
+}
+
+// One tracer round, entirely on the stream (no host synchronisation):
+// clear flags -> field of the current request list (count = counters[0])
+// -> near pass -> clear counters -> ctrl(consume E) -> surface distances
+// (count = counters[1]) -> ctrl(consume SD).  New E requests land in the
+// other list (r.ctrl.e_pts / e_line).
+cudaError_t launch_trace_round(const TraceRoundArgs& r, cudaStream_t st) {
+  const int L = r.ctrl.n_lines;
+  if (L == 0) return cudaSuccess;
+  cudaError_t e;
+  FieldArgs f = r.field;
+  int* flag = const_cast<int*>(r.ctrl.e_flag);
+  k_trace_reset_flags<<<min((L + 255) / 256, 148 * 4), 256, 0, st>>>(flag, L);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = launch_field_dyn(f, r.ctrl.counters, 148 * 12, st)) != cudaSuccess) return e;
+  k_trace_near<<<148 * 8, 128, 0, st>>>(r.ctrl.counters, f.split, f.pts, f.has_near, f.cls, r.nodes6, r.radii, f.tri_cols,
+                                        f.nt, r.u, r.duffy, r.n_duffy, r.graded, r.n_graded, r.bisect_depth,
+                                        r.bisect_trigger, r.prox, f.out, flag);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_trace_reset_counters<<<1, 32, 0, st>>>(r.ctrl.counters);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = launch_trace_ctrl(r.ctrl, 1, st)) != cudaSuccess) return e;
+  k_surface_distance<<<148 * 8, SD_THREADS, 0, st>>>(r.ctrl.sd_pts, 0, r.ctrl.counters + 1, r.ccr, f.nt, r.nodes6,
+                                                      const_cast<double*>(r.ctrl.sd_out));
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  return launch_trace_ctrl(r.ctrl, 2, st);
+}
+
 cudaError_t launch_trace_ctrl(const TraceArgs& a, int mode, cudaStream_t st) {
   if (a.n_lines == 0) return cudaSuccess;
   k_trace_ctrl<<<(a.n_lines + 127) / 128, 128, 0, st>>>(a, mode);
@@ -478,7 +597,7 @@ cudaError_t launch_trace_ctrl(const TraceArgs& a, int mode, cudaStream_t st) {
 cudaError_t launch_surface_distance(const double* pts, int m, const double* ccr, int nt, const double* nodes6,
                                     double* out, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
-  k_surface_distance<<<m, SD_THREADS, 0, st>>>(pts, m, ccr, nt, nodes6, out);
+  k_surface_distance<<<min(m, 148 * 8), SD_THREADS, 0, st>>>(pts, m, nullptr, ccr, nt, nodes6, out);
   return cudaGetLastError();
 }
 

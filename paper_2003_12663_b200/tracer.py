@@ -5,14 +5,17 @@ streamer integral 365-374).
 Every line is a state machine in HBM (csrc/trace.cu, ``LineState``).  The
 host drives *rounds*; per round it launches
 
+    k_field_dyn + reduce      ONE batched N-body over all requests
+    k_trace_near              per flagged target: near panels in index order
+                              (+ vertex-coincidence flags)
     k_trace_ctrl(mode=1)      consume E at each live line's last request
     k_surface_distance        lines that need d_surf(x) (once per step)
     k_trace_ctrl(mode=2)      consume d_surf, issue the next E request
-    field N-body (field.cu)   ONE batched evaluation over all requests
-                              (+ deferred near pairs, vertex-coincidence flags)
 
-and reads back three counters (E requests, SD requests, longest polyline).
-Lines therefore advance in lockstep, one field evaluation per round, and
+as ONE C-ABI call (hvb_trace_round) with every count kept on the device:
+rounds are enqueued back to back and the host reads the counters (pending
+requests, longest polyline) only every ROUNDS_PER_SYNC rounds.  Lines
+advance in lockstep, one field evaluation per round, and
 the control arithmetic -- stage points, error norm, accept / reject, step
 control, surface-hit arming and snapping, termination order -- is the
 reference's, statement by statement, on the device.
@@ -75,12 +78,15 @@ def surface_distance_device(dm, X_dev):
     return out
 
 
+ROUNDS_PER_SYNC = 16  # rounds enqueued between host reads of the counters
+
+
 def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap: int = 64,
                  max_rounds: int | None = None) -> TraceResult:
     import torch
 
     from .device import device_mesh
-    from .postprocess import _sources, _u_device, field_points_device
+    from .postprocess import _sources, _u_device, panel_split
 
     dm = device_mesh(mesh, cfg)
     dev = dm.device
@@ -94,15 +100,16 @@ def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap:
         raise ValueError(f"{L} start points but {orient.size} orientations")
     f64 = dict(dtype=torch.float64, device=dev)
     i32 = dict(dtype=torch.int32, device=dev)
+    n = max(1, L)
     sbytes = _lib.lib().hvb_line_state_bytes()
-    state = torch.zeros(max(1, L) * sbytes, dtype=torch.uint8, device=dev)
+    state = torch.zeros(n * sbytes, dtype=torch.uint8, device=dev)
     geo = np.ascontiguousarray(_geometry(mesh, params))  # host parameters (13 doubles)
     geo_p = geo.ctypes.data_as(ctypes.c_void_p)
     starts_d = torch.as_tensor(starts, **f64)
     orient_d = torch.as_tensor(np.where(orient >= 0, 1, -1).astype(np.int32), **i32)
-    cap = max(2, int(initial_cap))
-    poly = torch.empty((max(1, L), cap, 5), **f64)
-    n = max(1, L)
+    K = ROUNDS_PER_SYNC
+    cap = max(2 * K + 2, int(initial_cap))
+    poly = torch.empty((n, cap, 5), **f64)
     e_pts = [torch.empty((n, 3), **f64), torch.empty((n, 3), **f64)]
     e_line = [torch.empty(n, **i32), torch.empty(n, **i32)]
     sd_pts = torch.empty((n, 3), **f64)
@@ -110,46 +117,46 @@ def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap:
     sd_out = torch.empty((n, 2), **f64)
     e_out = torch.empty((n, 3), **f64)
     e_flag = torch.zeros(n, **i32)
-    counters = torch.zeros(3, dtype=torch.int64, device=dev)
-
-    def ctrl(mode, buf):
-        _lib.call("hvb_trace_ctrl", _lib.ptr(state), L, _lib.ptr(starts_d), _lib.ptr(orient_d), geo_p, mode,
-                  _lib.ptr(e_pts[buf]), _lib.ptr(e_line[buf]), _lib.ptr(sd_pts), _lib.ptr(sd_line),
-                  _lib.ptr(counters), _lib.ptr(e_out), _lib.ptr(e_flag), _lib.ptr(sd_out), _lib.ptr(poly), cap, st)
-
+    split = panel_split(dm.nt)
+    has_near = torch.zeros((split, n), **i32)  # chunk flags; the near pass clears what it reads
+    part = torch.empty((split, n, 4), **f64)
+    counters = torch.zeros(4, dtype=torch.int64, device=dev)
+    cfgq = dm.cfg
     rounds = 0
-    evals = 0
     if L:
-        ctrl(0, 0)
-    n_e, cur = L, 0
-    max_pts = 0
-    while n_e > 0 and (max_rounds is None or rounds < max_rounds):
-        rounds += 1
-        evals += n_e
-        # one batched field evaluation over every outstanding request
-        e_flag[:n_e].zero_()
-        E = field_points_device(dm, u_dev, src, e_pts[cur][:n_e], False, coincide_flag=e_flag)
-        e_out[:n_e].copy_(E)
-        if max_pts + 1 >= cap:  # at most one point is appended per line per round
-            new = torch.empty((L, 2 * cap, 5), **f64)
-            new[:, :cap] = poly
-            poly, cap = new, 2 * cap
-        counters.zero_()
-        nxt = 1 - cur
-        ctrl(1, nxt)
+        _lib.call("hvb_trace_ctrl", _lib.ptr(state), L, _lib.ptr(starts_d), _lib.ptr(orient_d), geo_p, 0,
+                  _lib.ptr(e_pts[0]), _lib.ptr(e_line[0]), _lib.ptr(sd_pts), _lib.ptr(sd_line),
+                  _lib.ptr(counters), _lib.ptr(e_out), _lib.ptr(e_flag), _lib.ptr(sd_out), _lib.ptr(poly), cap, st)
+    cur = 0
+    pending = L
+    while pending > 0 and (max_rounds is None or rounds < max_rounds):
+        for _ in range(K):
+            nxt = 1 - cur
+            _lib.call("hvb_trace_round", _lib.ptr(state), L, geo_p, _lib.ptr(e_pts[cur]), _lib.ptr(e_pts[nxt]),
+                      _lib.ptr(e_line[nxt]), _lib.ptr(sd_pts), _lib.ptr(sd_line), _lib.ptr(sd_out),
+                      _lib.ptr(counters), _lib.ptr(e_out), _lib.ptr(e_flag), _lib.ptr(has_near), _lib.ptr(part),
+                      _lib.ptr(src), _lib.ptr(dm.cls), _lib.ptr(dm.tri_cols), dm.nt, dm.nq, split,
+                      _lib.ptr(dm.nodes6), _lib.ptr(dm.radii), _lib.ptr(dm.ccr), _lib.ptr(u_dev),
+                      _lib.ptr(dm.rule_near), len(dm.rule_near), _lib.ptr(dm.rule_graded), len(dm.rule_graded),
+                      int(cfgq.bisect_depth), float(cfgq.bisect_trigger), VERTEX_PROXIMITY, _lib.ptr(poly), cap, st)
+            cur = nxt
+            rounds += 1
         c = counters.cpu().numpy()
-        if c[1]:
-            sd_out[: c[1]].copy_(surface_distance_device(dm, sd_pts[: c[1]]))
-            ctrl(2, nxt)
-            c = counters.cpu().numpy()
-        n_e, max_pts, cur = int(c[0]), int(c[2]), nxt
-        if _LOG and rounds % _LOG == 0:
-            print(f"[trace] round {rounds}: {n_e} requests, {int(c[1])} surface queries, longest {max_pts} points",
-                  flush=True)
+        pending, max_pts = int(c[0]), int(c[2])
+        if _LOG:
+            print(f"[trace] round {rounds}: {pending} requests, longest {max_pts} points", flush=True)
+        if pending and max_pts + K + 1 >= cap:  # at most one point per line per round
+            new_cap = cap
+            while max_pts + K + 1 >= new_cap:
+                new_cap *= 2
+            new = torch.empty((n, new_cap, 5), **f64)
+            new[:, :cap] = poly
+            poly, cap = new, new_cap
 
-    info = torch.empty((max(1, L), 4), **i32)
-    dinfo = torch.empty(max(1, L), **f64)
+    info = torch.empty((n, 4), **i32)
+    dinfo = torch.empty(n, **f64)
     _lib.call("hvb_trace_summary", _lib.ptr(state), L, _lib.ptr(info), _lib.ptr(dinfo), st)
+    evals = int(counters[3].item())
     return TraceResult(polylines=poly, info=info[:L].cpu().numpy(), start_mag=dinfo[:L].cpu().numpy(), state=state,
                        cap=cap, rounds=rounds, field_points=evals)
 
