@@ -160,11 +160,25 @@ _CPU_MESH = None
 EVALS_PER_LINE = 140.2  # field evaluations per traced cfg5 line (B200 run, tools/trace_probe.py 1.0 100000)
 
 
+_CPU_TABLES = None
+
+
+def _one_thread():
+    """Forked sample workers: one BLAS thread each (no oversubscription)."""
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(1)
+    except ImportError:  # pragma: no cover
+        pass
+
+
 def _cpu_rows(rows):
     from oracle import hvb_oracle as ora
 
+    _one_thread()
     t = time.perf_counter()
-    ora.row_equations(_CPU_MESH, rows)
+    ora.row_equations(_CPU_MESH, rows, tables=_CPU_TABLES)
     return time.perf_counter() - t
 
 
@@ -177,8 +191,12 @@ def cpu_sample(mesh, n_rows: int, processes: int, field_points: int = 4):
 
     from oracle import hvb_oracle as ora
 
-    global _CPU_MESH
-    _CPU_MESH = mesh
+    global _CPU_MESH, _CPU_TABLES
+    if _CPU_MESH is not mesh:
+        _CPU_MESH = mesh
+        # per-mesh sample tables, built once before forking (the reference
+        # caches them per mesh too, src/mesh.py:343-352)
+        _CPU_TABLES = ora.Tables(mesh, ora.DEFAULT_CFG["regular_order"])
     N = mesh.n_collocation + mesh.n_floating
     rows = np.linspace(0, mesh.n_collocation - 1, n_rows).astype(int)
     chunks = [rows[i::processes].tolist() for i in range(processes)]
@@ -230,6 +248,7 @@ def _cpu_field(P):
 
     from oracle import hvb_oracle as ora
 
+    _one_thread()
     ora.efield_points(_CPU_MESH, np.ones(_CPU_MESH.n_collocation), P)
 
 
@@ -247,7 +266,7 @@ def run_reference(args):
     vals = []
     samp = None
     for k in range(args.warmup + args.steps):
-        s = cpu_sample(mesh, max(cores, args.cpu_rows), cores, field_points=max(2, cores))
+        s = cpu_sample(mesh, max(4 * cores, args.cpu_rows), cores, field_points=max(2, cores))
         if k >= args.warmup:
             vals.append(s)
         samp = s

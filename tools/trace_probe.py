@@ -32,7 +32,7 @@ torch.cuda.synchronize()
 print("seeds", len(starts), f"{time.time()-t0:.1f}s", flush=True)
 gas = load_ionization_model(os.path.join(os.path.dirname(fixtures.__file__), "data", "air_demo.gas"))
 maxr = int(os.environ.get('MAXR', '0')) or None
-for rep in range(2):
+for rep in range(int(os.environ.get("REPS", "1"))):
     torch.cuda.synchronize()
     t1 = time.time()
     res = trace_device(sol, mesh, starts, orient, TraceParams(), QuadConfig(), max_rounds=maxr)
