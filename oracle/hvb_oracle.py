@@ -487,8 +487,8 @@ def gmres(A, b, restart=100, rel_tol=1e-8, max_iters=2000, row_equilibrate=True)
 # ---------------------------------------------------------------------------
 
 
-def efield_points(mesh, u, X, cfg=None):
-    rows, _ = kernel_rows(mesh, X, None, "efield", cfg=cfg)
+def efield_points(mesh, u, X, cfg=None, tables=None):
+    rows, _ = kernel_rows(mesh, X, None, "efield", cfg=cfg, tables=tables)
     return np.einsum("j,rjd->rd", np.asarray(u), rows)
 
 
@@ -550,7 +550,8 @@ def trace_line(mesh, u, start, orientation=1, rel_tol=1e-6, h_min_frac=1e-6, h_m
     """Dormand-Prince 5(4) on the unit tangent (postprocess.py:244-357).
     Returns (points (m,3), |E| (m,), arcs (m,), termination).  ``efield``
     overrides the field evaluator (default: oracle kernel rows)."""
-    ev = efield or (lambda p: efield_points(mesh, u, p[None], cfg)[0])
+    tab = Tables(mesh, {**DEFAULT_CFG, **(cfg or {})}["regular_order"])
+    ev = efield or (lambda p: efield_points(mesh, u, p[None], cfg, tab)[0])
     lo, hi = mesh.vertices.min(axis=0), mesh.vertices.max(axis=0)
     center, half = 0.5 * (lo + hi), 0.5 * (hi - lo) * bbox_factor
     diag = math.sqrt(ddot3(hi - lo, hi - lo))
