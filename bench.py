@@ -163,8 +163,14 @@ EVALS_PER_LINE = 140.2  # field evaluations per traced cfg5 line (B200 run, tool
 _CPU_TABLES = None
 
 
+_PARENT_PID = os.getpid()
+
+
 def _one_thread():
-    """Forked sample workers: one BLAS thread each (no oversubscription)."""
+    """Forked sample workers: one BLAS thread each (no oversubscription);
+    a no-op in the parent process."""
+    if os.getpid() == _PARENT_PID:
+        return
     try:
         from threadpoolctl import threadpool_limits
 
@@ -316,7 +322,7 @@ def run_b200(args):
     import __graft_entry__
 
     __graft_entry__.build()
-    from paper_2003_12663_b200 import _lib, assembly, fixtures, postprocess, tracer
+    from paper_2003_12663_b200 import _lib, assembly, device, fixtures, postprocess, tracer
     from paper_2003_12663_b200.quadrature import QuadConfig
     from paper_2003_12663_b200.assembly import assemble
     from paper_2003_12663_b200.device import device_mesh
@@ -532,9 +538,9 @@ def run_b200(args):
                       "rank0_max_points": trace_stats.get("max_points"),
                       "note": "cfg5 on the step's own solution: surface |E|, top-k seeds, sign(E.n) orientation, "
                               "device RK45 tracer + streamer (air_demo.gas)"},
-            "roofline": {"bound": "fp64", "kernel": "k_assemble_dual", "achieved": achieved,
+            "roofline": {"bound": "fp64", "kernel": f"k_assemble_{device.LAYOUT}", "achieved": achieved,
                          "peak": tflops_peak, "unit": "TFLOP/s", "frac": achieved / tflops_peak if tflops_peak else None,
-                         "traffic": _ncu_traffic("k_assemble_dual"), "peak_source": "measured DFMA kernel on this GPU (hvb_bench_dfma)"},
+                         "traffic": _ncu_traffic(f"k_assemble_{device.LAYOUT}"), "peak_source": "measured DFMA kernel on this GPU (hvb_bench_dfma)"},
             "roofline_gemv": {"bound": "hbm", "kernel": "k_gemv_f64", "traffic": _ncu_traffic("k_gemv"), "achieved": gemv_bytes / t_gemv / 1e9,
                               "peak": read_gbs, "unit": "GB/s", "frac": gemv_bytes / t_gemv / 1e9 / read_gbs,
                               "frac_of_measured_copy": gemv_bytes / t_gemv / 1e9 / 6547.2,
@@ -576,7 +582,7 @@ def _ncu_traffic(kernel="k_assemble_dual"):
             rec = json.load(fh).get(kernel)
     except (OSError, ValueError):
         return None
-    notes = {"k_assemble_dual": "one SL launch of the regular sweep (dominated by the matrix write)",
+    notes = {"k_assemble_row4": "one SL launch of the regular sweep (dominated by the matrix write)",
              "k_gemv": "one cfg4 matvec (the 79 GB row-major block is read once)"}
     return None if rec is None else {"bytes_per_launch": rec["bytes_per_launch"], "source": os.path.basename(files[-1]),
                                      "note": notes.get(kernel, "")}

@@ -35,13 +35,14 @@ int hvb_version(void);
  * Replaces: TriangleTables.__init__  assembly.py:78-103 */
 int hvb_build_table(const double* nodes6, int nt, int nq, const double* rule, double* table, void* stream);
 
-/* Pack the per-column-tile panel streams (one record of 6*nq+8 doubles per
- * (tile, panel) entry): sample table, circumcircle classification bracket
- * thr = fl(eta*R), owned local columns.  ent_meta = (mfirst, l0, l1, l2,
- * flags) per entry.  Replaces: the per-row classification setup of
- * row_pass1  assembly.py:155-168 */
+/* Pack the per-column-tile panel streams (one record per (tile, panel)
+ * entry): sample table, circumcircle classification bracket thr = fl(eta*R),
+ * owned local columns.  ent_meta = (mfirst, l0, l1, l2, flags) per entry.
+ * centered = 0: 6*nq+8 doubles, nodes (y, w0..2); centered = 1: 8*nq+8,
+ * nodes (-2(y-cc), |y-cc|^2, w0..2, 0) (row4 layouts).  Replaces: the
+ * per-row classification setup of row_pass1  assembly.py:155-168 */
 int hvb_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
-                     const int* ent_meta, long long n_entries, double* stream_out, void* stream);
+                     const int* ent_meta, long long n_entries, int centered, double* stream_out, void* stream);
 
 /* K2+K3 -- regular sweep of n_rows collocation rows against every panel,
  * classification fused (regular iff ||x-cc|| > eta*R with the reference's

@@ -40,9 +40,9 @@ int hvb_build_table(const double* nodes6, int nt, int nq, const double* rule, do
 }
 
 int hvb_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
-                     const int* ent_meta, long long n_entries, double* stream_out, void* stream) {
+                     const int* ent_meta, long long n_entries, int centered, double* stream_out, void* stream) {
   if (n_entries < 0) return fail(HVB_EARG, "hvb_build_stream: negative entry count");
-  return check(hvb::launch_build_stream(table, nq, ccr, eta, ent_tri, ent_meta, n_entries, stream_out,
+  return check(hvb::launch_build_stream(table, nq, ccr, eta, ent_tri, ent_meta, n_entries, centered, stream_out,
                                         (cudaStream_t)stream),
                "hvb_build_stream");
 }

@@ -29,28 +29,53 @@ __global__ void k_build_table(const double* __restrict__ nodes6, int nt, int nq,
 }
 
 // Pack one stream record per (tile, panel) entry.
+// centered = 0: per node (y, w0, w1, w2) -- 6 doubles (dual / quad layouts).
+// centered = 1: per node (-2 (y - cc), |y - cc|^2, w0, w1, w2, 0) -- 8 doubles
+// relative to the panel's circumcentre cc (row4 layouts): the kernel then
+// forms r^2 = |x-cc|^2 + |y-cc|^2 - 2 (x-cc).(y-cc) in 4 FP64 ops, with the
+// |x-cc|^2 it already needs for the classification.  Regular pairs have
+// |x-cc| > 1.2 R >= |y-cc| + 0.2 R, so the cancellation costs at most ~100 ulp
+// of r^2 (1e-14 relative).  The record tail (8 doubles) follows the nodes.
 __global__ void k_build_stream(const double* __restrict__ table, int nq,
                                const double* __restrict__ ccr,  // (nt,4): cc, R
                                double eta, const int* __restrict__ ent_tri,
                                const int* __restrict__ ent_meta,  // (ne,5): mfirst, slot0, slot1, slot2, flags
-                               int64_t ne, double* __restrict__ out) {
+                               int64_t ne, int centered, double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= ne) return;
-  const int rec = 6 * nq + 8;
+  const int per = centered ? 8 : 6;
+  const int rec = per * nq + 8;
   int t = ent_tri[e];
   double* o = out + e * rec;
   const double* s = table + (size_t)t * 6 * nq;
-  for (int k = 0; k < 6 * nq; ++k) o[k] = s[k];
   const double* c = ccr + 4 * (size_t)t;
+  if (centered) {
+    for (int q = 0; q < nq; ++q) {
+      const double* y = s + 6 * q;
+      const d3 yc = sub_rn(mk3(y[0], y[1], y[2]), mk3(c[0], c[1], c[2]));
+      double* oq = o + 8 * q;
+      oq[0] = -2.0 * yc.x;
+      oq[1] = -2.0 * yc.y;
+      oq[2] = -2.0 * yc.z;
+      oq[3] = sumsq_unfused(yc);
+      oq[4] = y[3];
+      oq[5] = y[4];
+      oq[6] = y[5];
+      oq[7] = 0.0;
+    }
+  } else {
+    for (int k = 0; k < 6 * nq; ++k) o[k] = s[k];
+  }
   double thr = __dmul_rn(eta, c[3]);
   double t2 = thr * thr;
-  o[6 * nq + 0] = c[0];
-  o[6 * nq + 1] = c[1];
-  o[6 * nq + 2] = c[2];
-  o[6 * nq + 3] = thr;
-  o[6 * nq + 4] = t2 * (1.0 - 1e-13);
-  o[6 * nq + 5] = t2 * (1.0 + 1e-13);
-  int* m = reinterpret_cast<int*>(o + 6 * nq + 6);
+  double* tail = o + per * nq;
+  tail[0] = c[0];
+  tail[1] = c[1];
+  tail[2] = c[2];
+  tail[3] = thr;
+  tail[4] = t2 * (1.0 - 1e-13);
+  tail[5] = t2 * (1.0 + 1e-13);
+  int* m = reinterpret_cast<int*>(tail + 6);
   const int* em = ent_meta + 5 * e;
   m[0] = t;
   m[1] = em[0];
@@ -134,10 +159,11 @@ cudaError_t launch_build_table(const double* nodes6, int nt, int nq, const doubl
 }
 
 cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, double eta,
-                                const int* ent_tri, const int* ent_meta, int64_t ne, double* out,
+                                const int* ent_tri, const int* ent_meta, int64_t ne, int centered, double* out,
                                 cudaStream_t st) {
   if (ne == 0) return cudaSuccess;
-  k_build_stream<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(table, nq, ccr, eta, ent_tri, ent_meta, ne, out);
+  k_build_stream<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(table, nq, ccr, eta, ent_tri, ent_meta, ne, centered,
+                                                              out);
   return cudaGetLastError();
 }
 

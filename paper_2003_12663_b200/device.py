@@ -41,6 +41,8 @@ LAYOUT = __import__("os").environ.get("HVB_ASM_LAYOUT", "row4")
 QUAD = LAYOUT in ("quad", "row4", "row8")
 GROUP = {"dual": 2, "quad": 4, "row4": 4, "row8": 8}[LAYOUT]
 LAYOUT_BITS = {"dual": 0, "quad": 8, "row4": 16, "row8": 32}[LAYOUT]
+# row layouts read circumcentre-centred panel records (csrc/tables.cu)
+CENTERED = LAYOUT in ("row4", "row8")
 MAX_TILE = int(__import__("os").environ.get("HVB_ASM_MAXTILE", "32767"))
 
 
@@ -244,10 +246,11 @@ class DeviceMesh:
         meta[:, 1:4] = np.where(loc >= 0, loc % WINDOW, WINDOW)  # window slots (WINDOW = dump slot)
         ent_meta = torch.as_tensor(meta, **i32).contiguous()
         ne = len(tiling.ent_tri)
-        self.rec = 6 * self.nq + 8
+        self.centered = CENTERED
+        self.rec = (8 if CENTERED else 6) * self.nq + 8
         self.stream = torch.empty((ne, self.rec), **f64)
         _lib.call("hvb_build_stream", _lib.ptr(self.table), self.nq, _lib.ptr(self.ccr), float(cfg.eta),
-                  _lib.ptr(ent_tri), _lib.ptr(ent_meta), ne, _lib.ptr(self.stream), st)
+                  _lib.ptr(ent_tri), _lib.ptr(ent_meta), ne, int(CENTERED), _lib.ptr(self.stream), st)
         self.n_tiles = len(tiling.tile_width)
 
 
