@@ -39,7 +39,8 @@ int hvb_build_table(const double* nodes6, int nt, int nq, const double* rule, do
  * entry): sample table, circumcircle classification bracket thr = fl(eta*R),
  * owned local columns.  ent_meta = (mfirst, l0, l1, l2, flags) per entry.
  * centered = 0: 6*nq+8 doubles, nodes (y, w0..2); centered = 1: 8*nq+8,
- * nodes (-2(y-cc), |y-cc|^2, w0..2, 0) (row4 layouts).  Replaces: the
+ * nodes (-2(y-cc), |y-cc|^2, w0..2, 0) (not used by the shipped layouts).
+ * Replaces: the
  * per-row classification setup of row_pass1  assembly.py:155-168 */
 int hvb_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
                      const int* ent_meta, long long n_entries, int centered, double* stream_out, void* stream);

@@ -1,8 +1,5 @@
 // Regular sweep (K2+K3), "row4" layout: lane = row (32 rows per warp), FOUR
 // panel records per lane per step (four independent FP64 chains per lane).
-// Records are circumcentre-centred (tables.cu, centered = 1): with x' = x - cc
-// and |x'|^2 from the classification, r^2 = |x'|^2 + |y'|^2 + x'.(-2y') costs
-// 4 FP64 ops per node instead of 6, i.e. 10 ops per SL node-row.
 // Unlike the quad layout every lane owns its window row exclusively, so the
 // window adds need no half-warp serialisation; each node's data feeds one
 // row instead of two (twice the shared-memory broadcast loads).  Same
@@ -40,7 +37,7 @@ HVB_DEV bool regular(double sq, const double* cg) {
 template <int NQ, int MODE, int WIN, int R>
 __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
   using namespace row4;
-  constexpr int REC = 8 * NQ + 8;  // circumcentre-centred records (tables.cu, centered = 1)
+  constexpr int REC = 6 * NQ + 8;
   constexpr int SREC = R * REC;
   constexpr int SLOTS = Shape<WIN>::SLOTS;
   constexpr int WREG = Shape<WIN>::WREG;
@@ -107,22 +104,10 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
     wait_group<1>();
     __syncwarp();
     const double* pr = ring + (p & 1) * SREC;
-    const int mfirst = reinterpret_cast<const int*>(pr + 8 * NQ + 6)[1];
+    const int mfirst = reinterpret_cast<const int*>(pr + 6 * NQ + 6)[1];
     while (mfirst >= base + 32) {
       flush32(base);
       base += 32;
-    }
-    // per record: x - cc, |x - cc|^2 (classification and r^2), (x - cc).n
-    d3 xc[R];
-    double x2[R], xn[R];
-    bool reg[R];
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const double* cg = pr + j * REC + 8 * NQ;
-      xc[j] = sub_rn(X0, mk3(cg[0], cg[1], cg[2]));
-      x2[j] = sumsq_unfused(xc[j]);
-      reg[j] = row4::regular(x2[j], cg);
-      xn[j] = (MODE == 0) ? 0.0 : fma(xc[j].z, N0.z, fma(xc[j].y, N0.y, xc[j].x * N0.x));
     }
     double acc[R][3];
 #pragma unroll
@@ -131,25 +116,24 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
     for (int q = 0; q < NQ; ++q) {
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        const double* nd = pr + j * REC + 8 * q;  // (-2(y-cc), |y-cc|^2, w0, w1, w2, 0)
-        const double2 a01 = *reinterpret_cast<const double2*>(nd);
-        const double2 a23 = *reinterpret_cast<const double2*>(nd + 2);
-        const double2 w01 = *reinterpret_cast<const double2*>(nd + 4);
-        const double w2 = nd[6];
-        const double r2 = fma(xc[j].z, a23.x, fma(xc[j].y, a01.y, fma(xc[j].x, a01.x, x2[j] + a23.y)));
+        const double* rec = pr + j * REC;
+        const double2 p01 = *reinterpret_cast<const double2*>(rec + 6 * q);
+        const double2 p2w = *reinterpret_cast<const double2*>(rec + 6 * q + 2);
+        const double2 w12 = *reinterpret_cast<const double2*>(rec + 6 * q + 4);
+        const double dx = X0.x - p01.x, dy = X0.y - p01.y, dz = X0.z - p2w.x;
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
         double k;
         if (MODE == 0) {  // 2/r: the flush applies the 1/2
           k = rsqrt2_newton(r2);
         } else {
           const double ri = rsqrt_full(r2);
-          const double yn = fma(a23.x, N0.z, fma(a01.y, N0.y, a01.x * N0.x));  // -2 (y-cc).n
-          const double dn = fma(0.5, yn, xn[j]);                               // (x-y).n
+          const double dn = fma(dz, N0.z, fma(dy, N0.y, dx * N0.x));
           const double t = dn * (ri * ri * ri);
           k = (MODE == 1) ? t : (adl0 ? t : ri);
         }
-        acc[j][0] = fma(k, w01.x, acc[j][0]);
-        acc[j][1] = fma(k, w01.y, acc[j][1]);
-        acc[j][2] = fma(k, w2, acc[j][2]);
+        acc[j][0] = fma(k, p2w.y, acc[j][0]);
+        acc[j][1] = fma(k, w12.x, acc[j][1]);
+        acc[j][2] = fma(k, w12.y, acc[j][2]);
       }
     }
     int slots[R][3];
@@ -158,9 +142,10 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
     bool any_emit = false;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      const double* cg = pr + j * REC + 8 * NQ;
+      const double* cg = pr + j * REC + 6 * NQ;
       const bool valid = R * p + j < ne;
-      if (!reg[j]) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
+      const bool reg = row4::regular(sumsq_unfused(sub_rn(X0, mk3(cg[0], cg[1], cg[2]))), cg);
+      if (!reg) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
       const int* meta = reinterpret_cast<const int*>(cg + 6);
       const unsigned sl = static_cast<unsigned>(meta[2]), sf = static_cast<unsigned>(meta[3]);
       slots[j][0] = valid ? (int)(sl & 0xffffu) : WIN;
@@ -168,7 +153,7 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
       slots[j][2] = valid ? (int)(sf & 0xffffu) : WIN;
       const bool prim = valid && (sf >> 16) & 1u;
       tris[j] = valid ? meta[0] : 0;
-      emit[j] = !reg[j] && prim && live0;
+      emit[j] = !reg && prim && live0;
       any_emit |= emit[j];
     }
     // deferred near pairs (rare): emitted from the panel's primary tile only
@@ -218,7 +203,7 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
 
 template <int WIN>
 static size_t row4_smem_bytes(int nq, int r) {
-  return (size_t)(row4::Shape<WIN>::WREG + row4::DEPTH * r * (8 * nq + 8)) * sizeof(double);
+  return (size_t)(row4::Shape<WIN>::WREG + row4::DEPTH * r * (6 * nq + 8)) * sizeof(double);
 }
 
 template <int NQ, int WIN, int R>

@@ -31,7 +31,8 @@ __global__ void k_build_table(const double* __restrict__ nodes6, int nt, int nq,
 // Pack one stream record per (tile, panel) entry.
 // centered = 0: per node (y, w0, w1, w2) -- 6 doubles (dual / quad layouts).
 // centered = 1: per node (-2 (y - cc), |y - cc|^2, w0, w1, w2, 0) -- 8 doubles
-// relative to the panel's circumcentre cc (row4 layouts): the kernel then
+// relative to the panel's circumcentre cc (measured for the row4 layout,
+// slower there -- device.py CENTERED): a kernel can then
 // forms r^2 = |x-cc|^2 + |y-cc|^2 - 2 (x-cc).(y-cc) in 4 FP64 ops, with the
 // |x-cc|^2 it already needs for the classification.  Regular pairs have
 // |x-cc| > 1.2 R >= |y-cc| + 0.2 R, so the cancellation costs at most ~100 ulp

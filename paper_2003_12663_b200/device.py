@@ -41,8 +41,11 @@ LAYOUT = __import__("os").environ.get("HVB_ASM_LAYOUT", "row4")
 QUAD = LAYOUT in ("quad", "row4", "row8")
 GROUP = {"dual": 2, "quad": 4, "row4": 4, "row8": 8}[LAYOUT]
 LAYOUT_BITS = {"dual": 0, "quad": 8, "row4": 16, "row8": 32}[LAYOUT]
-# row layouts read circumcentre-centred panel records (csrc/tables.cu)
-CENTERED = LAYOUT in ("row4", "row8")
+# circumcentre-centred panel records (csrc/tables.cu, centered = 1) save two
+# FP64 ops per node-row but need 8 doubles per node: the bigger ring drops
+# row4 to 9 resident warps/SM and it measured slower (0.365 vs 0.343 s on
+# cfg4), so every layout reads the plain 6-double records
+CENTERED = False
 MAX_TILE = int(__import__("os").environ.get("HVB_ASM_MAXTILE", "32767"))
 
 
