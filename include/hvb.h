@@ -51,7 +51,9 @@ int hvb_build_stream(const double* table, int nq, const double* ccr, double eta,
  * as row_scale * sum, for row-list entries [row_begin, row_begin+n_rows).
  * Non-regular, non-singular pairs are appended to
  * near_list as (row-list index, triangle).  mode: 0 all-SL, 1 all-ADL,
- * 2 mixed; | 4 = 64-column window (else 96); | 8 = quad layout (the panel
+ * 2 mixed; | W << 8 = W-column window (row4: 40, 48, 56, 64), else | 4 =
+ * 64-column window, else 96; | R << 16 = R records per lane (row layouts:
+ * 2, 3, 4 or 8; the stream band is bounded over groups of R). | 8 = quad layout (the panel
  * stream's band is bounded over groups of 4 records, else 2); | 16 = row4
  * layout (lane = row, 4 records per lane; same stream as quad); | 32 = row8
  * (8 records per lane, band over groups of 8).

@@ -358,7 +358,8 @@ def _run_rows(dm, plan: RowPlan, A, counts: dict, warps_per_block: int = 4):
                     "hvb_assemble_regular", _lib.ptr(dm.stream), _lib.ptr(dm.tile_ptr), _lib.ptr(dm.tile_col0),
                     _lib.ptr(dm.tile_width), dm.n_tiles, dm.nq, lo, hi - lo, _lib.ptr(plan.rowdata),
                     _lib.ptr(plan.kind), _lib.ptr(plan.col), _lib.ptr(plan.scale), _lib.ptr(plan.out),
-                    _lib.ptr(A), _lib.ptr(dm.tri_cols), mode | (4 if dm.window == 64 else 0) | dm.layout_bits, _WPB,
+                    _lib.ptr(A), _lib.ptr(dm.tri_cols), mode | (dm.window << 8 if dm.layout_bits & 48 else (4 if dm.window == 64 else 0)) | dm.layout_bits,
+                    _WPB,
                     _lib.ptr(near), _lib.ptr(cnt),
                     cap, s)
         n_near = int(cnt.item())

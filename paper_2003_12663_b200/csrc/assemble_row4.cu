@@ -236,6 +236,11 @@ cudaError_t launch_regular_row4(const RegularArgs& a, int nq, int mode, int wind
   };
   using I4 = std::integral_constant<int, 4>;
   using I8 = std::integral_constant<int, 8>;
+  if (window == 48 && r == 4) return pick(std::integral_constant<int, 48>{}, I4{});
+  if (window == 48 && r == 2) return pick(std::integral_constant<int, 48>{}, std::integral_constant<int, 2>{});
+  if (window == 48 && r == 3) return pick(std::integral_constant<int, 48>{}, std::integral_constant<int, 3>{});
+  if (window == 40 && r == 4) return pick(std::integral_constant<int, 40>{}, I4{});
+  if (window == 56 && r == 4) return pick(std::integral_constant<int, 56>{}, I4{});
   if (window == 64 && r == 8) return pick(std::integral_constant<int, 64>{}, I8{});
   if (window == 64 && r == 4) return pick(std::integral_constant<int, 64>{}, I4{});
   if (window == 96 && r == 4) return pick(std::integral_constant<int, 96>{}, I4{});

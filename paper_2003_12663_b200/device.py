@@ -29,9 +29,12 @@ from .quadrature import QuadConfig, duffy_rule, graded_rule, regular_rule
 __all__ = ["ColumnTiling", "column_tiling", "DeviceMesh", "device_mesh", "WINDOW_BAND"]
 
 WINDOW_BAND = 64  # csrc/assemble_dual.cu: WIN - 32 for the default 96-column window
-# regular-sweep window (96 or 64 columns) and tile shape; env overrides are
-# for A/B measurements (tools/ab.sh)
-WINDOW = int(__import__("os").environ.get("HVB_ASM_WIN", "64"))
+# regular-sweep window (row4: 40/48/56/64 columns, dual/quad: 64/96) and tile
+# shape; env overrides are for A/B measurements (tools/ab.sh).  Measured on
+# cfg4 (regular kernel): row4 x 48 columns 0.319 s, x 56 0.336, x 64 0.346,
+# x 40 0.360 (the window's shared memory sets the resident warps; a narrower
+# window means more tile-boundary panels: redundancy 1.14 at 64, 1.21 at 48)
+WINDOW = int(__import__("os").environ.get("HVB_ASM_WIN", "0"))  # 0: 48 for row4 (best on cfg4), else 64
 STRIPS = __import__("os").environ.get("HVB_ASM_STRIPS", "1") == "1"
 # quad layout (csrc/assemble_quad.cu: 2 records x 2 rows per lane) needs the
 # band bounded over groups of 4 records; the dual layout over groups of 2
@@ -39,8 +42,10 @@ STRIPS = __import__("os").environ.get("HVB_ASM_STRIPS", "1") == "1"
 # the same stream as quad
 LAYOUT = __import__("os").environ.get("HVB_ASM_LAYOUT", "row4")
 QUAD = LAYOUT in ("quad", "row4", "row8")
-GROUP = {"dual": 2, "quad": 4, "row4": 4, "row8": 8}[LAYOUT]
-LAYOUT_BITS = {"dual": 0, "quad": 8, "row4": 16, "row8": 32}[LAYOUT]
+RPL = int(__import__("os").environ.get("HVB_ASM_R", "0"))  # row layouts: records per lane (0 = default)
+GROUP = RPL if RPL and LAYOUT == "row4" else {"dual": 2, "quad": 4, "row4": 4, "row8": 8}[LAYOUT]
+LAYOUT_BITS = {"dual": 0, "quad": 8, "row4": 16, "row8": 32}[LAYOUT] | ((RPL << 16) if LAYOUT == "row4" else 0)
+WINDOW = WINDOW or (48 if LAYOUT == "row4" else 64)
 # circumcentre-centred panel records (csrc/tables.cu, centered = 1) save two
 # FP64 ops per node-row but need 8 doubles per node: the bigger ring drops
 # row4 to 9 resident warps/SM and it measured slower (0.365 vs 0.343 s on
