@@ -348,9 +348,12 @@ def run_b200(args):
     counter = {"n": 0}
     orig_call = _lib.call
 
+    # kernels launched per C-ABI call (1 unless listed)
+    per_call = {"hvb_trace_round": 8}  # flag reset, N-body, split reduce, near pass, counter reset, ctrl, SD, ctrl
+
     def counting_call(name, *a):
         if not name.startswith("hvb_bench"):
-            counter["n"] += 1
+            counter["n"] += per_call.get(name, 1)
         return orig_call(name, *a)
 
     _lib.call = counting_call
