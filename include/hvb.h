@@ -111,10 +111,14 @@ int hvb_contract(const double* table, int nt, int nq, const int* tri_cols, const
                  void* stream);
 
 /* K10/K11 -- N-body potential (potential=1) or field at m points over the
- * regular panels; panel range split `split` ways into part (split, m, 4);
- * near pairs appended as (point, triangle).
+ * regular panels; panel range split `split` ways (on 32-panel group
+ * boundaries) into part (split, m, 4); near pairs appended as (point,
+ * triangle).  groups: (ceil(nt/32), 8) bounds of aligned 32-panel groups
+ * (centre, rho_cls, rho_sd): a group farther than rho_cls is regular as a
+ * whole, which skips its per-panel classification.
  * Replaces: eval_potential / eval_efield  postprocess.py:112-133 */
-int hvb_field(const double* src, const double* cls, const int* tri_cols, int nt, int nq, const double* pts,
+int hvb_field(const double* src, const double* cls, const double* groups, const int* tri_cols, int nt, int nq,
+              const double* pts,
               const int* own_col, int m, int split, int potential, double* part, int* near_list,
               unsigned long long* near_count, long long near_cap, void* stream);
 
@@ -163,7 +167,7 @@ int hvb_trace_ctrl(void* state, int n_lines, const double* starts, const int* or
 int hvb_trace_round(void* state, int n_lines, const double* geo, double* cur_pts, double* nxt_pts, int* nxt_line,
                     double* sd_pts, int* sd_line, double* sd_out, unsigned long long* counters, double* e_out,
                     int* e_flag, int* has_near, double* part, const double* src, const double* cls,
-                    const int* tri_cols, int nt, int nq, int split, const double* nodes6, const double* radii,
+                    const double* groups, const int* tri_cols, int nt, int nq, int split, const double* nodes6, const double* radii,
                     const double* ccr, const double* u, const double* duffy, int n_duffy, const double* graded,
                     int n_graded, int bisect_depth, double bisect_trigger, double prox, double* out_pts, int cap,
                     void* stream);
@@ -176,8 +180,8 @@ int hvb_trace_summary(const void* state, int n_lines, int* info, double* dinfo, 
  * at m points: 12 circumcircle candidates ranked by ||x-cc||-R, flat
  * closest point mapped through the quadratic patch, first minimum wins.
  * out (m, 2).  Replaces: _surface_distance  postprocess.py:198-218 */
-int hvb_surface_distance(const double* pts, int m, const double* ccr, int nt, const double* nodes6, double* out,
-                         void* stream);
+int hvb_surface_distance(const double* pts, int m, const double* ccr, const double* groups, int nt,
+                         const double* nodes6, double* out, void* stream);
 
 /* flag[i] = 1 for near-pair targets within prox of a node of the pair's
  * panel.  Replaces: _check_point  postprocess.py:104-109 for tracer

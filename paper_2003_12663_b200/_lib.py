@@ -33,15 +33,15 @@ SIGNATURES = {
     "hvb_gather_scale": [_P, _P, _P, _I, _P, _P],
     "hvb_rowmax_diag": [_P, _I, _LL, _I, _I, _P, _P, _P, _P],
     "hvb_contract": [_P, _I, _I, _P, _P, _P, _P],
-    "hvb_field": [_P, _P, _P, _I, _I, _P, _P, _I, _I, _I, _P, _P, _P, _LL, _P],
+    "hvb_field": [_P, _P, _P, _P, _I, _I, _P, _P, _I, _I, _I, _P, _P, _P, _LL, _P],
     "hvb_field_reduce": [_P, _I, _I, _P, _P],
     "hvb_near_apply_points": [_P, _I, _P, _P, _P, _P, _I, _P, _P],
     "hvb_field_singular": [_P, _P, _P, _P, _P, _P, _I, _P, _P, _P, _I, _P, _D, _P, _P, _P],
     "hvb_trace_ctrl": [_P, _I, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P],
     "hvb_trace_summary": [_P, _I, _P, _P, _P],
-    "hvb_trace_round": [_P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P,
-                        _P, _I, _P, _I, _I, _D, _D, _P, _I, _P],
-    "hvb_surface_distance": [_P, _I, _P, _I, _P, _P, _P],
+    "hvb_trace_round": [_P, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P,
+                        _P, _P, _I, _P, _I, _I, _D, _D, _P, _I, _P],
+    "hvb_surface_distance": [_P, _I, _P, _P, _I, _P, _P, _P],
     "hvb_near_coincide": [_P, _LL, _P, _P, _D, _P, _P],
     "hvb_streamer": [_P, _P, _I, _I, _P, _P, _I, _D, _P, _P, _P],
     "hvb_bench_dfma": [_P, _I, _I, _P],

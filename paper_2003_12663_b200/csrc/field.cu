@@ -46,8 +46,10 @@ HVB_DEV void field_tile(const FieldArgs& a, int bx, int by, double2* s_src, doub
   const int tt = live ? ti : a.m - 1;
   const d3 X = mk3(a.pts[3 * (size_t)tt], a.pts[3 * (size_t)tt + 1], a.pts[3 * (size_t)tt + 2]);
   const int own = a.own_col ? a.own_col[tt] : -1;
-  const int tb = (int)((long long)a.nt * by / a.split);
-  const int te = (int)((long long)a.nt * (by + 1) / a.split);
+  // split boundaries on FCH-panel group boundaries (group bounds, below)
+  const int ng = (a.nt + FCH - 1) / FCH;
+  const int tb = min(a.nt, FCH * (int)((long long)ng * by / a.split));
+  const int te = min(a.nt, FCH * (int)((long long)ng * (by + 1) / a.split));
   double ex = 0.0, ey = 0.0, ez = 0.0;
   bool any_near = false;
   for (int c0 = tb; c0 < te; c0 += FCH) {
@@ -58,9 +60,14 @@ HVB_DEV void field_tile(const FieldArgs& a, int bx, int by, double2* s_src, doub
     for (int k = tid; k < cn * 6; k += FT) s_cls[k] = a.cls[(size_t)c0 * 6 + k];
     for (int k = tid; k < cn * 3; k += FT) s_cols[k] = a.tri_cols[(size_t)c0 * 3 + k];
     __syncthreads();
+    // whole group far from the target: every panel is regular (exactly;
+    // device.py panel_groups) -- skip the per-panel classification
+    const double* gb = a.groups + 8 * (size_t)(c0 / FCH);
+    const double gd = __dsqrt_rn(sumsq_unfused(sub_rn(X, mk3(gb[0], gb[1], gb[2]))));
+    const bool far = gd > gb[3] * (1.0 + 1e-12);
     for (int j = 0; j < cn; ++j) {
       const double* c = s_cls + 6 * j;
-      const bool reg = is_regular(X, mk3(c[0], c[1], c[2]), c[3], c[4], c[5]);
+      const bool reg = far || is_regular(X, mk3(c[0], c[1], c[2]), c[3], c[4], c[5]);
       double fx = 0.0, fy = 0.0, fz = 0.0;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {

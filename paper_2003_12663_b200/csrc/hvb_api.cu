@@ -173,13 +173,15 @@ int hvb_contract(const double* table, int nt, int nq, const int* tri_cols, const
   return check(hvb::launch_contract(table, nt, nq, tri_cols, u, src, (cudaStream_t)stream), "hvb_contract");
 }
 
-int hvb_field(const double* src, const double* cls, const int* tri_cols, int nt, int nq, const double* pts,
+int hvb_field(const double* src, const double* cls, const double* groups, const int* tri_cols, int nt, int nq,
+              const double* pts,
               const int* own_col, int m, int split, int potential, double* part, int* near_list,
               unsigned long long* near_count, long long near_cap, void* stream) {
   if (split < 1) return fail(HVB_EARG, "hvb_field: split must be >= 1");
   hvb::FieldArgs a;
   a.src = src;
   a.cls = cls;
+  a.groups = groups;
   a.tri_cols = tri_cols;
   a.nt = nt;
   a.nq = nq;
@@ -257,7 +259,7 @@ int hvb_trace_ctrl(void* state, int n_lines, const double* starts, const int* or
 int hvb_trace_round(void* state, int n_lines, const double* geo, double* cur_pts, double* nxt_pts, int* nxt_line,
                     double* sd_pts, int* sd_line, double* sd_out, unsigned long long* counters, double* e_out,
                     int* e_flag, int* has_near, double* part, const double* src, const double* cls,
-                    const int* tri_cols, int nt, int nq, int split, const double* nodes6, const double* radii,
+                    const double* groups, const int* tri_cols, int nt, int nq, int split, const double* nodes6, const double* radii,
                     const double* ccr, const double* u, const double* duffy, int n_duffy, const double* graded,
                     int n_graded, int bisect_depth, double bisect_trigger, double prox, double* out_pts, int cap,
                     void* stream) {
@@ -292,6 +294,7 @@ int hvb_trace_round(void* state, int n_lines, const double* geo, double* cur_pts
   hvb::FieldArgs& f = r.field;
   f.src = src;
   f.cls = cls;
+  f.groups = groups;
   f.tri_cols = tri_cols;
   f.nt = nt;
   f.nq = nq;
@@ -326,10 +329,10 @@ int hvb_trace_summary(const void* state, int n_lines, int* info, double* dinfo, 
                "hvb_trace_summary");
 }
 
-int hvb_surface_distance(const double* pts, int m, const double* ccr, int nt, const double* nodes6, double* out,
-                         void* stream) {
+int hvb_surface_distance(const double* pts, int m, const double* ccr, const double* groups, int nt,
+                         const double* nodes6, double* out, void* stream) {
   if (m < 0 || nt < 1) return fail(HVB_EARG, "hvb_surface_distance: bad m/nt");
-  return check(hvb::launch_surface_distance(pts, m, ccr, nt, nodes6, out, (cudaStream_t)stream),
+  return check(hvb::launch_surface_distance(pts, m, ccr, groups, nt, nodes6, out, (cudaStream_t)stream),
                "hvb_surface_distance");
 }
 

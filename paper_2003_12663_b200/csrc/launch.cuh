@@ -66,6 +66,7 @@ struct NearArgs {
 struct FieldArgs {
   const double* src;      // (nt, nq, 4) contracted sources
   const double* cls;      // (nt, 6): cc, thr, thr2_lo, thr2_hi
+  const double* groups;   // (ceil(nt/32), 8): bounds of aligned 32-panel groups (device.py panel_groups)
   const int* tri_cols;    // (nt, 3) original cols (singular test)
   int nt, nq;
   const double* pts;      // (m, 3) targets
@@ -172,8 +173,8 @@ struct TraceRoundArgs {
 
 cudaError_t launch_trace_ctrl(const TraceArgs& a, int mode, cudaStream_t st);
 cudaError_t launch_trace_round(const TraceRoundArgs& r, cudaStream_t st);
-cudaError_t launch_surface_distance(const double* pts, int m, const double* ccr, int nt, const double* nodes6,
-                                    double* out, cudaStream_t st);
+cudaError_t launch_surface_distance(const double* pts, int m, const double* ccr, const double* groups, int nt,
+                                    const double* nodes6, double* out, cudaStream_t st);
 cudaError_t launch_near_coincide(const int* pairs, long long n_pairs, const double* pts, const double* nodes6,
                                  double prox, int* flag, cudaStream_t st);
 cudaError_t launch_trace_summary(const LineState* state, int n_lines, int* info, double* dinfo, cudaStream_t st);

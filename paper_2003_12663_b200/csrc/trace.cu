@@ -311,9 +311,15 @@ constexpr int SD_THREADS = 256;
 constexpr int SD_K = 12;
 
 // m_dev != nullptr: the query count is read on the device (tracer rounds)
+// Threads take whole aligned 32-panel groups; a group whose lower bound
+// ||x - C|| - rho_sd (device.py panel_groups, with a 1e-12 relative margin)
+// is not below the thread's current 12th key cannot insert and is skipped.
+// The top-12 set is (key, index) ordered, so it does not depend on the
+// visiting order.
 __global__ void __launch_bounds__(SD_THREADS) k_surface_distance(const double* __restrict__ pts, int m_host,
                                                                  const unsigned long long* m_dev,
-                                                                 const double* __restrict__ ccr, int nt,
+                                                                 const double* __restrict__ ccr,
+                                                                 const double* __restrict__ groups, int nt,
                                                                  const double* __restrict__ nodes6,
                                                                  double* __restrict__ out) {
   __shared__ double s_key[SD_THREADS * SD_K];
@@ -332,7 +338,13 @@ __global__ void __launch_bounds__(SD_THREADS) k_surface_distance(const double* _
     key[k] = INFINITY;
     idx[k] = 0x7fffffff;
   }
-  for (int t = tid; t < nt; t += SD_THREADS) {
+  const int ng = (nt + 31) / 32;
+  for (int g = tid; g < ng; g += SD_THREADS) {
+    const double* gb = groups + 8 * (size_t)g;
+    const double gd = __dsqrt_rn(sumsq_unfused(sub_rn(X, mk3(gb[0], gb[1], gb[2]))));
+    if (gd - gb[4] - 1e-12 * (gd + gb[4]) >= key[SD_K - 1]) continue;
+    const int tend = min(nt, 32 * g + 32);
+  for (int t = 32 * g; t < tend; ++t) {
     const double* c = ccr + 4 * (size_t)t;
     const double lower = __dsub_rn(__dsqrt_rn(sumsq_unfused(sub_rn(X, mk3(c[0], c[1], c[2])))), c[3]);
     if (lower < key[SD_K - 1]) {  // t increases: ties keep the earlier panel
@@ -350,6 +362,7 @@ __global__ void __launch_bounds__(SD_THREADS) k_surface_distance(const double* _
       }
     }
   }
+  }  // groups
 #pragma unroll
   for (int k = 0; k < SD_K; ++k) {
     s_key[tid * SD_K + k] = key[k];
@@ -510,8 +523,9 @@ __global__ void k_trace_near(const unsigned long long* m_dev, int split, const d
           e1 = E[3 * (size_t)i + 1];
           e2 = E[3 * (size_t)i + 2];
         }
-        const int tb = (int)((long long)nt * chunk / split);
-        const int te = (int)((long long)nt * (chunk + 1) / split);
+        const int ngr = (nt + 31) / 32;  // chunk bounds as in field.cu field_tile
+        const int tb = min(nt, 32 * (int)((long long)ngr * chunk / split));
+        const int te = min(nt, 32 * (int)((long long)ngr * (chunk + 1) / split));
         for (int t0 = tb; t0 < te; t0 += 32) {
           const int t = t0 + lane;
           bool nr = false;
@@ -582,7 +596,8 @@ cudaError_t launch_trace_round(const TraceRoundArgs& r, cudaStream_t st) {
   k_trace_reset_counters<<<1, 32, 0, st>>>(r.ctrl.counters);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = launch_trace_ctrl(r.ctrl, 1, st)) != cudaSuccess) return e;
-  k_surface_distance<<<148 * 8, SD_THREADS, 0, st>>>(r.ctrl.sd_pts, 0, r.ctrl.counters + 1, r.ccr, f.nt, r.nodes6,
+  k_surface_distance<<<148 * 8, SD_THREADS, 0, st>>>(r.ctrl.sd_pts, 0, r.ctrl.counters + 1, r.ccr, f.groups, f.nt,
+                                                      r.nodes6,
                                                       const_cast<double*>(r.ctrl.sd_out));
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   return launch_trace_ctrl(r.ctrl, 2, st);
@@ -594,10 +609,10 @@ cudaError_t launch_trace_ctrl(const TraceArgs& a, int mode, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_surface_distance(const double* pts, int m, const double* ccr, int nt, const double* nodes6,
-                                    double* out, cudaStream_t st) {
+cudaError_t launch_surface_distance(const double* pts, int m, const double* ccr, const double* groups, int nt,
+                                    const double* nodes6, double* out, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
-  k_surface_distance<<<min(m, 148 * 8), SD_THREADS, 0, st>>>(pts, m, nullptr, ccr, nt, nodes6, out);
+  k_surface_distance<<<min(m, 148 * 8), SD_THREADS, 0, st>>>(pts, m, nullptr, ccr, groups, nt, nodes6, out);
   return cudaGetLastError();
 }
 

@@ -220,6 +220,7 @@ class DeviceMesh:
         thr = cfg.eta * mesh.circumradii
         cls = np.column_stack([mesh.circumcenters, thr, thr * thr * (1 - 1e-13), thr * thr * (1 + 1e-13)])
         self.cls = torch.as_tensor(cls, **f64).contiguous()
+        self.groups = torch.as_tensor(panel_groups(mesh.circumcenters, mesh.circumradii, thr), **f64).contiguous()
 
         # rule tables
         reg = regular_rule(cfg.regular_order)
@@ -260,6 +261,32 @@ class DeviceMesh:
         _lib.call("hvb_build_stream", _lib.ptr(self.table), self.nq, _lib.ptr(self.ccr), float(cfg.eta),
                   _lib.ptr(ent_tri), _lib.ptr(ent_meta), ne, int(CENTERED), _lib.ptr(self.stream), st)
         self.n_tiles = len(tiling.tile_width)
+
+
+PANEL_GROUP = 32  # csrc/field.cu FCH: panels per shared-memory batch / bound group
+
+
+def panel_groups(cc: np.ndarray, radii: np.ndarray, thr: np.ndarray) -> np.ndarray:
+    """Bounding data of aligned groups of PANEL_GROUP consecutive panels,
+    (n_groups, 8) = centre (3), rho_cls, rho_sd, pad: every panel t of the
+    group satisfies ||cc_t - C|| + fl(eta R_t) <= rho_cls and ||cc_t - C|| +
+    R_t <= rho_sd (inflated by 1e-12 relative).  A target with ||x - C|| >
+    rho_cls (1 + 1e-12) classifies every panel of the group regular, and
+    ||x - C|| - rho_sd bounds the group's surface-distance keys from below
+    -- both exactly, far beyond FP64 rounding (csrc/field.cu, trace.cu)."""
+    nt = len(cc)
+    ng = -(-nt // PANEL_GROUP)
+    pad = ng * PANEL_GROUP - nt
+    idx = np.concatenate([np.arange(nt), np.full(pad, nt - 1)]).reshape(ng, PANEL_GROUP)
+    c = cc[idx]                              # (ng, G, 3)
+    lo, hi = c.min(axis=1), c.max(axis=1)
+    C = 0.5 * (lo + hi)
+    d = np.sqrt(((c - C[:, None, :]) ** 2).sum(axis=2))
+    out = np.zeros((ng, 8))
+    out[:, :3] = C
+    out[:, 3] = (d + thr[idx]).max(axis=1) * (1.0 + 1e-12)
+    out[:, 4] = (d + radii[idx]).max(axis=1) * (1.0 + 1e-12)
+    return out
 
 
 def mesh_tiling(mesh, max_tile: int = 2048, window: int = 96, strips: bool = False, group: int = 2) -> ColumnTiling:

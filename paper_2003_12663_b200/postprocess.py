@@ -209,7 +209,8 @@ def _field_points(dm, u_dev, src, X_dev, potential: bool, own_col=None, coincide
     while True:
         near = torch.empty((cap, 2), dtype=torch.int32, device=dev)
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-        _lib.call("hvb_field", _lib.ptr(src), _lib.ptr(dm.cls), _lib.ptr(dm.tri_cols), dm.nt, dm.nq,
+        _lib.call("hvb_field", _lib.ptr(src), _lib.ptr(dm.cls), _lib.ptr(dm.groups), _lib.ptr(dm.tri_cols), dm.nt,
+                  dm.nq,
                   _lib.ptr(X_dev), _lib.ptr(own_col), m, split, int(potential), _lib.ptr(part), _lib.ptr(near),
                   _lib.ptr(cnt), cap, s)
         n_near = int(cnt.item())

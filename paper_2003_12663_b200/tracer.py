@@ -73,7 +73,8 @@ def surface_distance_device(dm, X_dev):
     m = int(X_dev.shape[0])
     out = torch.empty((m, 2), dtype=torch.float64, device=dm.device)
     if m:
-        _lib.call("hvb_surface_distance", _lib.ptr(X_dev), m, _lib.ptr(dm.ccr), dm.nt, _lib.ptr(dm.nodes6),
+        _lib.call("hvb_surface_distance", _lib.ptr(X_dev), m, _lib.ptr(dm.ccr), _lib.ptr(dm.groups), dm.nt,
+                  _lib.ptr(dm.nodes6),
                   _lib.ptr(out), _lib.stream_ptr(dm.device))
     return out
 
@@ -135,7 +136,8 @@ def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap:
             _lib.call("hvb_trace_round", _lib.ptr(state), L, geo_p, _lib.ptr(e_pts[cur]), _lib.ptr(e_pts[nxt]),
                       _lib.ptr(e_line[nxt]), _lib.ptr(sd_pts), _lib.ptr(sd_line), _lib.ptr(sd_out),
                       _lib.ptr(counters), _lib.ptr(e_out), _lib.ptr(e_flag), _lib.ptr(has_near), _lib.ptr(part),
-                      _lib.ptr(src), _lib.ptr(dm.cls), _lib.ptr(dm.tri_cols), dm.nt, dm.nq, split,
+                      _lib.ptr(src), _lib.ptr(dm.cls), _lib.ptr(dm.groups), _lib.ptr(dm.tri_cols), dm.nt, dm.nq,
+                      split,
                       _lib.ptr(dm.nodes6), _lib.ptr(dm.radii), _lib.ptr(dm.ccr), _lib.ptr(u_dev),
                       _lib.ptr(dm.rule_near), len(dm.rule_near), _lib.ptr(dm.rule_graded), len(dm.rule_graded),
                       int(cfgq.bisect_depth), float(cfgq.bisect_trigger), VERTEX_PROXIMITY, _lib.ptr(poly), cap, st)

@@ -198,7 +198,7 @@ def test_assemble_vs_oracle_random_points(cases):
 
 def test_regular_sweep_layouts(cases, monkeypatch):
     """The default layout is deterministic (bitwise on re-assembly), and the
-    quad layout (uncentred records, same 4-record tiling) agrees to rounding."""
+    quad layout (64-column window, its own tiling) agrees to rounding."""
     from oracle import hvb_oracle as ora
     from paper_2003_12663_b200 import device
     from paper_2003_12663_b200.assembly import assemble
@@ -208,6 +208,7 @@ def test_regular_sweep_layouts(cases, monkeypatch):
     np.testing.assert_array_equal(a, assemble(m)[0].toarray())
     m._device_cache.clear()
     monkeypatch.setattr(device, "LAYOUT_BITS", 8)
+    monkeypatch.setattr(device, "WINDOW", 64)
     monkeypatch.setattr(device, "CENTERED", False)
     monkeypatch.setattr(device, "GROUP", 4)
     b = assemble(m)[0].toarray()
