@@ -144,7 +144,7 @@ int hvb_field_singular(const double* nodes6, const int* tri_cols, const int* vc_
  * request slots); mode 2 consumes surface distances (sd_out).  New E / SD
  * requests are appended to e_pts/e_line and sd_pts/sd_line through
  * counters[0] / counters[1]; counters[2] = max points per line, counters[3] =
- * total E requests; polylines (n_lines, cap, 5) = x, y, z, |E|, s.
+ * total E requests, counters[4] = N-body work counter (6 entries); polylines (n_lines, cap, 5) = x, y, z, |E|, s.
  * Replaces: trace_fieldline  postprocess.py:244-357 (control flow, step
  * control, surface-hit snapping, termination order) */
 int hvb_line_state_bytes(void);

@@ -135,16 +135,26 @@ __global__ void __launch_bounds__(FT) k_field(FieldArgs a) {
 // loop over (target block, split) items: launchable without knowing the
 // count on the host (the tracer's sync-free rounds).  part is (split, m, 4)
 // with the row stride of the CURRENT count.
+// Items are handed out through an atomic work counter (m_dev[4], zeroed
+// before the launch), so every SM stays busy until the last item whatever
+// the count -- the per-target sums do not depend on which CTA runs them.
 template <int NQ>
-__global__ void __launch_bounds__(FT) k_field_dyn(FieldArgs a, const unsigned long long* m_dev) {
+__global__ void __launch_bounds__(FT) k_field_dyn(FieldArgs a, unsigned long long* m_dev) {
   __shared__ double2 s_src[FCH * NQ * 2];
   __shared__ double s_cls[FCH * 6];
   __shared__ int s_cols[FCH * 3];
-  a.m = (int)*m_dev;
+  __shared__ long long s_item;
+  a.m = (int)m_dev[0];
   const int nb = (a.m + FT - 1) / FT;
   const long long items = (long long)nb * a.split;
-  for (long long it = blockIdx.x; it < items; it += gridDim.x)
+  while (true) {
+    if (threadIdx.x == 0) s_item = (long long)atomicAdd(m_dev + 4, 1ull);
+    __syncthreads();
+    const long long it = s_item;
+    __syncthreads();
+    if (it >= items) break;
     field_tile<NQ, 0>(a, (int)(it % nb), (int)(it / nb), s_src, s_cls, s_cols);
+  }
 }
 
 // fixed-order reduction of the panel splits, count on the device
@@ -282,7 +292,7 @@ cudaError_t launch_contract(const double* table, int nt, int nq, const int* tri_
   return cudaGetLastError();
 }
 
-cudaError_t launch_field_dyn(const FieldArgs& a, const unsigned long long* m_dev, int grid, cudaStream_t st) {
+cudaError_t launch_field_dyn(const FieldArgs& a, unsigned long long* m_dev, int grid, cudaStream_t st) {
   switch (a.nq) {
     case 3: k_field_dyn<3><<<grid, FT, 0, st>>>(a, m_dev); break;
     case 6: k_field_dyn<6><<<grid, FT, 0, st>>>(a, m_dev); break;

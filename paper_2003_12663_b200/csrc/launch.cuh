@@ -103,7 +103,7 @@ cudaError_t launch_gather_scale(const double* z, const double* right, const int*
 cudaError_t launch_rowmax_diag(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const int* diag_col,
                                double* rowmax, double* diag, cudaStream_t st);
 cudaError_t launch_field(const FieldArgs& a, cudaStream_t st);
-cudaError_t launch_field_dyn(const FieldArgs& a, const unsigned long long* m_dev, int grid, cudaStream_t st);
+cudaError_t launch_field_dyn(const FieldArgs& a, unsigned long long* m_dev, int grid, cudaStream_t st);
 cudaError_t launch_contract(const double* table, int nt, int nq, const int* tri_cols, const double* u, double* src,
                             cudaStream_t st);
 cudaError_t launch_field_reduce(const double* part, int split, int m, double* out, cudaStream_t st);
@@ -142,7 +142,8 @@ struct TraceArgs {
   double* sd_pts;         // (n_lines, 3)
   int* sd_line;
   unsigned long long* counters;  // [0] E requests, [1] SD requests, [2] max points per line,
-                                 // [3] total E requests (never reset)
+                                 // [3] total E requests (never reset), [4] N-body work
+                                 // counter (zeroed each round)
   // results of the previous requests
   const double* e_out;    // (n_req, 3)
   const int* e_flag;      // (n_req) 1 = coincident with a mesh vertex

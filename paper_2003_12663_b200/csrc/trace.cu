@@ -567,7 +567,8 @@ __global__ void k_trace_near(const unsigned long long* m_dev, int split, const d
   }
 }
 
-__global__ void k_trace_reset_flags(int* flag, int n) {
+__global__ void k_trace_reset_flags(int* flag, int n, unsigned long long* counters) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) counters[4] = 0;  // N-body work counter
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) flag[k] = 0;
 }
 
@@ -586,9 +587,9 @@ cudaError_t launch_trace_round(const TraceRoundArgs& r, cudaStream_t st) {
   cudaError_t e;
   FieldArgs f = r.field;
   int* flag = const_cast<int*>(r.ctrl.e_flag);
-  k_trace_reset_flags<<<min((L + 255) / 256, 148 * 4), 256, 0, st>>>(flag, L);
+  k_trace_reset_flags<<<min((L + 255) / 256, 148 * 4), 256, 0, st>>>(flag, L, r.ctrl.counters);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if ((e = launch_field_dyn(f, r.ctrl.counters, 148 * 12, st)) != cudaSuccess) return e;
+  if ((e = launch_field_dyn(f, r.ctrl.counters, 148 * 16, st)) != cudaSuccess) return e;
   k_trace_near<<<148 * 8, 128, 0, st>>>(r.ctrl.counters, f.split, f.pts, f.has_near, f.cls, r.nodes6, r.radii, f.tri_cols,
                                         f.nt, r.u, r.duffy, r.n_duffy, r.graded, r.n_graded, r.bisect_depth,
                                         r.bisect_trigger, r.prox, f.out, flag);

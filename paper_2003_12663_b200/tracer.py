@@ -121,7 +121,7 @@ def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap:
     split = panel_split(dm.nt)
     has_near = torch.zeros((split, n), **i32)  # chunk flags; the near pass clears what it reads
     part = torch.empty((split, n, 4), **f64)
-    counters = torch.zeros(4, dtype=torch.int64, device=dev)
+    counters = torch.zeros(6, dtype=torch.int64, device=dev)  # csrc/launch.cuh TraceArgs.counters
     cfgq = dm.cfg
     rounds = 0
     if L:
