@@ -101,6 +101,16 @@ int hvb_gemv(const void* A, int is_f32, long long lda, int n_rows, int n_cols, c
 /* xp[k] = z[perm[k]] / right[perm[k]]  (perm/right may be NULL) */
 int hvb_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp, void* stream);
 
+/* K9 -- one Arnoldi orthogonalisation in one cooperative launch: modified
+ * Gram-Schmidt of w (n) against rows V[0..j] (row pitch ldv) in order,
+ * h[i] = V_i.w (accumulate = 1: h[i] += for the re-orthogonalisation pass),
+ * norms = (||w|| before, ||w|| after); partial is scratch of
+ * hvb_mgs_partial_size() doubles.  Deterministic (fixed slices, CTA-order
+ * sums).  Replaces: the MGS loop of _gmres_cycle  solver.py:177-196 */
+int hvb_mgs_partial_size(void);
+int hvb_mgs(const double* V, long long ldv, int j, double* w, int n, double* h, double* norms, double* partial,
+            int accumulate, void* stream);
+
 /* K9 -- row max |a_ij| and diagonal.  Replaces: solver.py:98-107,
  * SystemMatrix.diagonal assembly.py:348-353 */
 int hvb_rowmax_diag(const void* A, int is_f32, long long lda, int n_rows, int n_cols, const int* diag_col,

@@ -32,6 +32,7 @@ SIGNATURES = {
     "hvb_gemv": [_P, _I, _LL, _I, _I, _P, _P, _P, _P],
     "hvb_gather_scale": [_P, _P, _P, _I, _P, _P],
     "hvb_rowmax_diag": [_P, _I, _LL, _I, _I, _P, _P, _P, _P],
+    "hvb_mgs": [_P, _LL, _I, _P, _I, _P, _P, _P, _I, _P],
     "hvb_contract": [_P, _I, _I, _P, _P, _P, _P],
     "hvb_field": [_P, _P, _P, _P, _I, _I, _P, _P, _I, _I, _I, _P, _P, _P, _LL, _P],
     "hvb_field_reduce": [_P, _I, _I, _P, _P],
@@ -87,6 +88,8 @@ def lib():
             h.hvb_version.restype = _I
             h.hvb_line_state_bytes.restype = _I
             h.hvb_line_state_bytes.argtypes = []
+            h.hvb_mgs_partial_size.restype = _I
+            h.hvb_mgs_partial_size.argtypes = []
             _lib = h
     return _lib
 

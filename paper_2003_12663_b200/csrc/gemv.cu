@@ -11,6 +11,8 @@
 // loads.  The per-row summation order depends only on N and the thread
 // count, never on the row blocking: results are bitwise identical for any
 // block partition (reference invariance, tests/test_assembly.py:72-78).
+#include <cooperative_groups.h>
+
 #include "launch.cuh"
 
 namespace hvb {
@@ -179,6 +181,100 @@ cudaError_t launch_rowmax_diag(const void* A, int is_f32, int64_t lda, int nrows
   else
     k_rowmax_diag<double><<<nrows, 256, 0, st>>>((const double*)A, lda, nrows, ncols, diag_col, rowmax, diag);
   return cudaGetLastError();
+}
+
+}  // namespace hvb
+
+// ---------------------------------------------------------------------------
+// K9: Arnoldi orthogonalisation of one GMRES step in ONE cooperative launch
+// (reference _gmres_cycle src/solver.py:177-196): modified Gram-Schmidt of w
+// against V[0..j] -- for i = 0..j: h_i = V_i . w; w -= h_i V_i -- plus the
+// norms before and after.  Each CTA owns a fixed contiguous slice of the N
+// entries; a projection's partial dots are written per CTA, the grid syncs,
+// and every CTA sums the partials in CTA order, so h_i (and w) are identical
+// on every CTA and bitwise reproducible.  accumulate = 1 adds the
+// projections to h (the reference's single re-orthogonalisation pass).
+// ---------------------------------------------------------------------------
+namespace hvb {
+namespace cgk = cooperative_groups;
+
+constexpr int MGS_THREADS = 256;
+
+HVB_DEV double block_sum(double v, double* s_red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) s_red[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (wid == 0) {
+    t = lane < (MGS_THREADS >> 5) ? s_red[lane] : 0.0;
+    t = warp_sum(t);
+  }
+  return t;  // valid in warp 0
+}
+
+__global__ void __launch_bounds__(MGS_THREADS) k_mgs(const double* __restrict__ V, long long ldv, int j,
+                                                     double* __restrict__ w, int n, double* __restrict__ h,
+                                                     double* __restrict__ norms, double* __restrict__ partial,
+                                                     int accumulate) {
+  cgk::grid_group grid = cgk::this_grid();
+  __shared__ double s_red[MGS_THREADS / 32];
+  __shared__ double s_val;
+  const int nb = gridDim.x;
+  const int chunk = (n + nb - 1) / nb;
+  const int a = min(n, blockIdx.x * chunk), b = min(n, a + chunk);
+  auto grid_total = [&](double v, int slot) {
+    const double t = block_sum(v, s_red);
+    if (threadIdx.x == 0) partial[(size_t)slot * nb + blockIdx.x] = t;
+    grid.sync();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int k = 0; k < nb; ++k) s += partial[(size_t)slot * nb + k];
+      s_val = s;
+    }
+    __syncthreads();
+    return s_val;
+  };
+  double loc = 0.0;
+  for (int k = a + threadIdx.x; k < b; k += MGS_THREADS) loc = fma(w[k], w[k], loc);
+  const double nb2 = grid_total(loc, 0);
+  for (int i = 0; i <= j; ++i) {
+    const double* vi = V + (size_t)i * ldv;
+    loc = 0.0;
+    for (int k = a + threadIdx.x; k < b; k += MGS_THREADS) loc = fma(vi[k], w[k], loc);
+    const double hi = grid_total(loc, 1 + (i & 1));  // alternating slots: no overwrite race
+    for (int k = a + threadIdx.x; k < b; k += MGS_THREADS) w[k] = fma(-hi, vi[k], w[k]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) h[i] = accumulate ? h[i] + hi : hi;
+  }
+  loc = 0.0;
+  for (int k = a + threadIdx.x; k < b; k += MGS_THREADS) loc = fma(w[k], w[k], loc);
+  const double na2 = grid_total(loc, 3);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    norms[0] = sqrt(nb2);
+    norms[1] = sqrt(na2);
+  }
+}
+
+int mgs_grid() {
+  static int g = 0;
+  if (g == 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mgs, MGS_THREADS, 0);
+    g = sms * (per < 2 ? per : 2);
+    if (g < 1) g = 1;
+  }
+  return g;
+}
+
+cudaError_t launch_mgs(const double* V, long long ldv, int j, double* w, int n, double* h, double* norms,
+                       double* partial, int accumulate, cudaStream_t st) {
+  const int grid = mgs_grid();
+  void* args[] = {(void*)&V, (void*)&ldv, (void*)&j, (void*)&w, (void*)&n, (void*)&h, (void*)&norms,
+                  (void*)&partial, (void*)&accumulate};
+  return cudaLaunchCooperativeKernel((void*)k_mgs, grid, MGS_THREADS, args, 0, st);
 }
 
 }  // namespace hvb

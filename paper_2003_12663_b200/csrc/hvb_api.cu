@@ -161,6 +161,14 @@ int hvb_gather_scale(const double* z, const double* right, const int* perm, int 
   return check(hvb::launch_gather_scale(z, right, perm, n, xp, (cudaStream_t)stream), "hvb_gather_scale");
 }
 
+int hvb_mgs_partial_size(void) { return 4 * hvb::mgs_grid(); }
+
+int hvb_mgs(const double* V, long long ldv, int j, double* w, int n, double* h, double* norms, double* partial,
+            int accumulate, void* stream) {
+  if (j < 0 || n <= 0 || ldv < n) return fail(HVB_EARG, "hvb_mgs: bad j/n/ldv");
+  return check(hvb::launch_mgs(V, ldv, j, w, n, h, norms, partial, accumulate, (cudaStream_t)stream), "hvb_mgs");
+}
+
 int hvb_rowmax_diag(const void* A, int is_f32, long long lda, int n_rows, int n_cols, const int* diag_col,
                     double* rowmax, double* diag, void* stream) {
   return check(hvb::launch_rowmax_diag(A, is_f32, lda, n_rows, n_cols, diag_col, rowmax, diag,

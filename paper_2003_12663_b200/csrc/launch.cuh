@@ -100,6 +100,9 @@ cudaError_t launch_gemv(const void* A, int is_f32, int64_t lda, int nrows, int n
                         const double* left, double* y, cudaStream_t st);
 cudaError_t launch_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp,
                                 cudaStream_t st);
+cudaError_t launch_mgs(const double* V, long long ldv, int j, double* w, int n, double* h, double* norms,
+                       double* partial, int accumulate, cudaStream_t st);
+int mgs_grid();
 cudaError_t launch_rowmax_diag(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const int* diag_col,
                                double* rowmax, double* diag, cudaStream_t st);
 cudaError_t launch_field(const FieldArgs& a, cudaStream_t st);
