@@ -1,0 +1,101 @@
+"""Edge cases of the device path: empty batches, dimension mismatches,
+bad arguments through the C ABI, the LeftDomain / MaxLength terminations,
+a one-panel-per-surface mesh, and determinism of repeated launches."""
+
+import numpy as np
+import pytest
+
+from conftest import build_case, gpu_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_ok(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def sphere():
+    from paper_2003_12663_b200 import fixtures
+    from paper_2003_12663_b200.assembly import assemble
+    from paper_2003_12663_b200.solver import SolverConfig, solve
+
+    m = fixtures.sphere_mesh(2)
+    A, rhs = assemble(m)
+    return m, A, rhs, solve(A, rhs, SolverConfig(rel_tol=1e-12))
+
+
+def test_empty_batches(sphere):
+    from paper_2003_12663_b200.postprocess import eval_efield_batch, eval_potential_batch, surface_distance_batch
+
+    m, _, _, sol = sphere
+    assert eval_efield_batch(sol, m, np.zeros((0, 3))).shape == (0, 3)
+    assert eval_potential_batch(sol, m, np.zeros((0, 3))).shape == (0,)
+    d, r = surface_distance_batch(m, np.zeros((0, 3)))
+    assert d.shape == (0,) and r.shape == (0,)
+
+
+def test_dimension_mismatches(sphere):
+    from paper_2003_12663_b200.assembly import AssemblyError, assemble, matvec
+    from paper_2003_12663_b200.solver import residual, solve
+
+    m, A, rhs, _ = sphere
+    with pytest.raises(ValueError):
+        matvec(A, np.ones(A.size + 1))
+    with pytest.raises(ValueError):
+        solve(A, rhs[:-1])
+    with pytest.raises(ValueError):
+        residual(A, np.ones(3), rhs)
+    with pytest.raises(ValueError):
+        solve(np.ones((3, 4)), np.ones(3))
+    with pytest.raises(AssemblyError):
+        assemble(m, precision="half")
+
+
+def test_c_abi_bad_arguments_raise_value_error():
+    import torch
+
+    from paper_2003_12663_b200 import _lib
+
+    with pytest.raises(ValueError, match="split"):
+        _lib.call("hvb_field", None, None, None, None, 10, 12, None, None, 1, 0, 0, None, None, None, 0,
+                  _lib.stream_ptr())
+    with pytest.raises(ValueError, match="nt/nq"):
+        _lib.call("hvb_build_table", None, 5, 7, None, None, _lib.stream_ptr())
+    torch.cuda.synchronize()
+
+
+def test_left_domain_and_max_length(sphere):
+    from paper_2003_12663_b200.postprocess import TraceParams, trace_fieldlines
+
+    m, _, _, sol = sphere
+    lines = trace_fieldlines(sol, m, np.array([[1.3, 0.1, 0.0], [1.3, 0.1, 0.0]]), [1, 1],
+                             params=None)
+    assert lines[0].termination == "LeftDomain"
+    np.testing.assert_array_equal(lines[0].points, lines[1].points)  # identical lines in one batch
+    short = trace_fieldlines(sol, m, np.array([[1.3, 0.1, 0.0]]), [1], params=TraceParams(max_length_frac=0.05))[0]
+    assert short.termination == "MaxLength"
+    # inward orientation from outside the sphere ends on the surface
+    hit = trace_fieldlines(sol, m, np.array([[1.3, 0.1, 0.0]]), [-1])[0]
+    assert hit.termination == "SurfaceHit" and abs(np.linalg.norm(hit.points[-1]) - 1.0) < 0.02
+
+
+def test_minimal_mesh_one_panel_per_surface():
+    from paper_2003_12663_b200.assembly import assemble
+    from paper_2003_12663_b200.mesh import parse_mesh
+    from paper_2003_12663_b200.solver import SolverConfig, solve
+
+    text = ("bemesh 1\nvertex 0 0 0 0\nvertex 1 1 0 0\nvertex 2 0 1 0\nvertex 3 0.5 0 0\n"
+            "vertex 4 0.5 0.5 0\nvertex 5 0 0.5 0\ntriangle 0 1 2 3 4 5 0\npatch 0 electrode 1.0\n")
+    m = parse_mesh(text)
+    A, rhs = assemble(m)
+    sol = solve(A, rhs, SolverConfig(rel_tol=1e-12))
+    assert A.shape == (3, 3) and np.all(np.isfinite(sol.u)) and np.all(sol.u > 0)
+
+
+def test_repeated_launches_bitwise(sphere):
+    from paper_2003_12663_b200.assembly import assemble
+    from paper_2003_12663_b200.postprocess import eval_efield_batch
+
+    m, A, _, sol = sphere
+    np.testing.assert_array_equal(A.toarray(), assemble(m)[0].toarray())
+    P = np.random.default_rng(4).uniform(-2, 2, (257, 3))
+    np.testing.assert_array_equal(eval_efield_batch(sol, m, P), eval_efield_batch(sol, m, P))
+    # a point evaluated alone equals the same point inside a batch
+    np.testing.assert_array_equal(eval_efield_batch(sol, m, P[100:101])[0], eval_efield_batch(sol, m, P)[100])
