@@ -78,3 +78,66 @@ def test_distributed_gmres_matches_single(N):
     x, it, _ = ora.gmres(A, b, restart=7, rel_tol=1e-12, max_iters=400)
     assert np.max(np.abs(u0 - x)) <= 1e-10 * np.max(np.abs(x))
     assert abs(it0 - it) <= 1
+
+
+def _gpu_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)  # ranks share cuda:0 here
+    try:
+        torch.cuda.set_device(0)
+        from paper_2003_12663_b200 import fixtures
+        from paper_2003_12663_b200.parallel import assemble_distributed, split_range
+        from paper_2003_12663_b200.postprocess import eval_efield_batch, trace_fieldlines
+        from paper_2003_12663_b200.solver import SolverConfig, solve
+
+        m = fixtures.concentric_mesh(2, [(0.5, "electrode 1.0"), (1.0, "electrode 0.0")])
+        A, rhs = assemble_distributed(m)
+        sol = solve(A, rhs, SolverConfig(rel_tol=1e-12))
+        P = np.array([[0.7, 0.1, 0.05], [0.1, 0.6, 0.2], [0.0, 0.0, 0.8], [0.55, 0.2, -0.3]])
+        a, b = split_range(len(P), world, rank)
+        E = eval_efield_batch(sol, m, P[a:b])
+        starts = np.array([[0.55, 0.0, 0.0], [0.0, 0.6, 0.0], [0.0, 0.0, -0.7]])
+        la, lb = split_range(len(starts), world, rank)
+        lines = trace_fieldlines(sol, m, starts[la:lb], [1] * (lb - la))
+        out_q.put((rank, sol.u, sol.iterations, E, [ln.points for ln in lines]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+def test_row_sharded_device_path_matches_single_process():
+    """World-size 2 (gloo; both ranks on cuda:0) through the real device
+    path: row-block assembly, all-gathered GMRES, points and lines split
+    per rank -- bitwise the single-process results."""
+    from paper_2003_12663_b200 import fixtures
+    from paper_2003_12663_b200.assembly import assemble
+    from paper_2003_12663_b200.postprocess import eval_efield_batch, trace_fieldlines
+    from paper_2003_12663_b200.solver import SolverConfig, solve
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+    m = fixtures.concentric_mesh(2, [(0.5, "electrode 1.0"), (1.0, "electrode 0.0")])
+    A, rhs = assemble(m)
+    sol = solve(A, rhs, SolverConfig(rel_tol=1e-12))
+    P = np.array([[0.7, 0.1, 0.05], [0.1, 0.6, 0.2], [0.0, 0.0, 0.8], [0.55, 0.2, -0.3]])
+    E = eval_efield_batch(sol, m, P)
+    starts = np.array([[0.55, 0.0, 0.0], [0.0, 0.6, 0.0], [0.0, 0.0, -0.7]])
+    lines = trace_fieldlines(sol, m, starts, [1, 1, 1])
+    for r in res:
+        np.testing.assert_allclose(r[1], sol.u, rtol=0, atol=1e-13 * np.max(np.abs(sol.u)))
+        assert abs(r[2] - sol.iterations) <= 1
+    np.testing.assert_allclose(np.vstack([r[3] for r in res]), E, rtol=1e-12, atol=1e-14)
+    got = [pts for r in res for pts in r[4]]
+    assert len(got) == len(lines)
+    for g, ln in zip(got, lines):
+        assert g.shape == ln.points.shape
+        np.testing.assert_allclose(g, ln.points, rtol=0, atol=1e-10)
