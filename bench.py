@@ -322,7 +322,7 @@ def run_b200(args):
     import __graft_entry__
 
     __graft_entry__.build()
-    from paper_2003_12663_b200 import _lib, assembly, device, fixtures, postprocess, tracer
+    from paper_2003_12663_b200 import _lib, assembly, device, fixtures, parallel, postprocess, tracer
     from paper_2003_12663_b200.quadrature import QuadConfig
     from paper_2003_12663_b200.assembly import assemble
     from paper_2003_12663_b200.device import device_mesh
@@ -531,7 +531,8 @@ def run_b200(args):
             "config": {"workload": f"cfg4 rod-plane+insulator: {nt} panels, N={N} (dense {8 * N * N / 1e9:.1f} GB FP64)",
                        "panels": nt, "N": N, "field_points": args.points, "scale": args.scale,
                        "l2": "inputs larger than L2 (matrix streamed every matvec)",
-                       "parallelism": f"row-block x{world}"},
+                       "parallelism": f"row-block x{world}",
+                       "matvec_exchange": (parallel.LAST_GATHER if world > 1 else None)},
             "gmres_solve_s": t_solve,
             "gmres_iterations": iters,
             "field_evals_per_s": args.points / t_field,

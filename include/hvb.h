@@ -98,6 +98,31 @@ int hvb_near_apply_rows(const int* seg_ptr, int n_seg, const int* pairs, const d
 int hvb_gemv(const void* A, int is_f32, long long lda, int n_rows, int n_cols, const double* x, const double* left,
              double* y, void* stream);
 
+/* Fused GEMV + all-gather (row-sharded GMRES): as hvb_gemv
+ * (f64), but each row result left[i] (A xp)_i is stored into all n_out
+ * replicated vectors outs[k][out_off + i] -- this GPU's and every peer's,
+ * mapped by CUDA IPC -- instead of a local y.  outs is a DEVICE array of
+ * n_out pointers.  Replaces: matvec + the NCCL all-gather of the row
+ * blocks (parallel.RowGather) */
+int hvb_gemv_bcast(const double* A, long long lda, int n_rows, int n_cols, const double* x, const double* left,
+                   double* const* outs, int n_out, long long out_off, void* stream);
+
+/* CUDA IPC plumbing for the peer buffers: a cudaMalloc'd (zeroed) region,
+ * its handle (hvb_ipc_handle_bytes() bytes), and a peer's mapping. */
+int hvb_ipc_alloc(long long bytes, void** ptr);
+int hvb_ipc_free(void* ptr);
+int hvb_ipc_handle_bytes(void);
+int hvb_ipc_handle(void* ptr, unsigned char* out);
+int hvb_ipc_open(const unsigned char* handle, void** ptr);
+int hvb_ipc_close(void* ptr);
+
+/* Cross-GPU epoch barrier over peer memory: signal writes `epoch` into slot
+ * `rank` of every rank's flag row (flags: DEVICE array of world pointers),
+ * after a system-scope fence; wait spins until every slot of this rank's
+ * flag row reached `epoch`. */
+int hvb_peer_signal(unsigned long long* const* flags, int world, int rank, unsigned long long epoch, void* stream);
+int hvb_peer_wait(const unsigned long long* flags, int world, unsigned long long epoch, void* stream);
+
 /* xp[k] = z[perm[k]] / right[perm[k]]  (perm/right may be NULL) */
 int hvb_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp, void* stream);
 

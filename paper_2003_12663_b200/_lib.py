@@ -31,6 +31,14 @@ SIGNATURES = {
     "hvb_near_apply_rows": [_P, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "hvb_gemv": [_P, _I, _LL, _I, _I, _P, _P, _P, _P],
     "hvb_gather_scale": [_P, _P, _P, _I, _P, _P],
+    "hvb_gemv_bcast": [_P, _LL, _I, _I, _P, _P, _P, _I, _LL, _P],
+    "hvb_ipc_alloc": [_LL, _P],
+    "hvb_ipc_free": [_P],
+    "hvb_ipc_handle": [_P, _P],
+    "hvb_ipc_open": [_P, _P],
+    "hvb_ipc_close": [_P],
+    "hvb_peer_signal": [_P, _I, _I, ctypes.c_ulonglong, _P],
+    "hvb_peer_wait": [_P, _I, ctypes.c_ulonglong, _P],
     "hvb_rowmax_diag": [_P, _I, _LL, _I, _I, _P, _P, _P, _P],
     "hvb_mgs": [_P, _LL, _I, _P, _I, _P, _P, _P, _I, _P],
     "hvb_contract": [_P, _I, _I, _P, _P, _P, _P],
@@ -90,6 +98,8 @@ def lib():
             h.hvb_line_state_bytes.argtypes = []
             h.hvb_mgs_partial_size.restype = _I
             h.hvb_mgs_partial_size.argtypes = []
+            h.hvb_ipc_handle_bytes.restype = _I
+            h.hvb_ipc_handle_bytes.argtypes = []
             _lib = h
     return _lib
 

@@ -239,9 +239,8 @@ def _rowmax_diag(st: DeviceStore):
     return rowmax, diag
 
 
-def device_matvec(st: DeviceStore, z, right=None, left=None, out=None):
-    """y = left .* (A (z ./ right)) on the device; z/right/left in original
-    order (torch float64 tensors)."""
+def gather_operand(st: DeviceStore, z, right=None):
+    """xp = (z ./ right) in the store's device column order."""
     import torch
 
     dev = st.A.device
@@ -254,6 +253,17 @@ def device_matvec(st: DeviceStore, z, right=None, left=None, out=None):
         if st.size > st.n:
             zt = z[st.n:]
             xp[st.n:] = zt / right[st.n:] if right is not None else zt
+    return xp
+
+
+def device_matvec(st: DeviceStore, z, right=None, left=None, out=None):
+    """y = left .* (A (z ./ right)) on the device; z/right/left in original
+    order (torch float64 tensors)."""
+    import torch
+
+    dev = st.A.device
+    xp = gather_operand(st, z, right)
+    s = _lib.stream_ptr(dev)
     rows = st.A.shape[0]
     y = out if out is not None else torch.empty(rows, dtype=torch.float64, device=dev)
     _lib.call("hvb_gemv", _lib.ptr(st.A), int(st.is_f32), st.lda, rows, st.size, _lib.ptr(xp),

@@ -19,11 +19,15 @@ namespace hvb {
 
 constexpr int GEMV_THREADS = 256;
 
+// outs != nullptr: the fused all-gather -- each row result is stored into
+// all n_out replicated vectors (this GPU's and every peer's, mapped over
+// NVLink by CUDA IPC) at position out_off + row, instead of into y.
 template <int ROWS>
 __global__ void __launch_bounds__(GEMV_THREADS) k_gemv_f64(const double* __restrict__ A, int64_t lda, int nrows,
                                                            int ncols, const double* __restrict__ x,
                                                            const double* __restrict__ left,
-                                                           double* __restrict__ y) {
+                                                           double* __restrict__ y, double* const* outs, int n_out,
+                                                           int64_t out_off) {
   const int r0 = blockIdx.x * ROWS;
   const int tid = threadIdx.x;
   double acc[ROWS];
@@ -66,7 +70,12 @@ __global__ void __launch_bounds__(GEMV_THREADS) k_gemv_f64(const double* __restr
     double s = 0.0;
 #pragma unroll
     for (int w = 0; w < GEMV_THREADS / 32; ++w) s += red[tid][w];
-    y[r0 + tid] = left ? left[r0 + tid] * s : s;
+    const double v = left ? left[r0 + tid] * s : s;
+    if (outs) {
+      for (int k = 0; k < n_out; ++k) outs[k][out_off + r0 + tid] = v;
+    } else {
+      y[r0 + tid] = v;
+    }
   }
 }
 
@@ -162,7 +171,16 @@ cudaError_t launch_gemv(const void* A, int is_f32, int64_t lda, int nrows, int n
   if (is_f32)
     k_gemv_f32<R><<<grid, GEMV_THREADS, 0, st>>>((const float*)A, lda, nrows, ncols, x, left, y);
   else
-    k_gemv_f64<R><<<grid, GEMV_THREADS, 0, st>>>((const double*)A, lda, nrows, ncols, x, left, y);
+    k_gemv_f64<R><<<grid, GEMV_THREADS, 0, st>>>((const double*)A, lda, nrows, ncols, x, left, y, nullptr, 0, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemv_bcast(const double* A, int64_t lda, int nrows, int ncols, const double* x, const double* left,
+                              double* const* outs, int n_out, int64_t out_off, cudaStream_t st) {
+  if (nrows == 0) return cudaSuccess;
+  constexpr int R = 8;
+  dim3 grid((nrows + R - 1) / R);
+  k_gemv_f64<R><<<grid, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, left, nullptr, outs, n_out, out_off);
   return cudaGetLastError();
 }
 

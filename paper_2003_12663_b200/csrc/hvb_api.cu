@@ -157,6 +157,49 @@ int hvb_gemv(const void* A, int is_f32, long long lda, int n_rows, int n_cols, c
   return check(hvb::launch_gemv(A, is_f32, lda, n_rows, n_cols, x, left, y, (cudaStream_t)stream), "hvb_gemv");
 }
 
+int hvb_gemv_bcast(const double* A, long long lda, int n_rows, int n_cols, const double* x, const double* left,
+                   double* const* outs, int n_out, long long out_off, void* stream) {
+  if (n_out < 1 || out_off < 0) return fail(HVB_EARG, "hvb_gemv_bcast: bad n_out/out_off");
+  return check(hvb::launch_gemv_bcast(A, lda, n_rows, n_cols, x, left, outs, n_out, out_off, (cudaStream_t)stream),
+               "hvb_gemv_bcast");
+}
+
+int hvb_ipc_alloc(long long bytes, void** ptr) {
+  if (bytes <= 0 || !ptr) return fail(HVB_EARG, "hvb_ipc_alloc: bad size");
+  cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaMemset(*ptr, 0, (size_t)bytes);
+  return check(e, "hvb_ipc_alloc");
+}
+
+int hvb_ipc_free(void* ptr) { return check(cudaFree(ptr), "hvb_ipc_free"); }
+
+int hvb_ipc_handle(void* ptr, unsigned char* out) {
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e == cudaSuccess) memcpy(out, &h, sizeof h);
+  return check(e, "hvb_ipc_handle");
+}
+
+int hvb_ipc_handle_bytes(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+int hvb_ipc_open(const unsigned char* handle, void** ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  return check(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "hvb_ipc_open");
+}
+
+int hvb_ipc_close(void* ptr) { return check(cudaIpcCloseMemHandle(ptr), "hvb_ipc_close"); }
+
+int hvb_peer_signal(unsigned long long* const* flags, int world, int rank, unsigned long long epoch, void* stream) {
+  if (world < 1 || world > 32 || rank < 0 || rank >= world) return fail(HVB_EARG, "hvb_peer_signal: bad world/rank");
+  return check(hvb::launch_peer_signal(flags, world, rank, epoch, (cudaStream_t)stream), "hvb_peer_signal");
+}
+
+int hvb_peer_wait(const unsigned long long* flags, int world, unsigned long long epoch, void* stream) {
+  if (world < 1 || world > 32) return fail(HVB_EARG, "hvb_peer_wait: bad world");
+  return check(hvb::launch_peer_wait(flags, world, epoch, (cudaStream_t)stream), "hvb_peer_wait");
+}
+
 int hvb_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp, void* stream) {
   return check(hvb::launch_gather_scale(z, right, perm, n, xp, (cudaStream_t)stream), "hvb_gather_scale");
 }

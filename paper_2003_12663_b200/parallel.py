@@ -8,8 +8,12 @@ PAPER.md:203 distributes the same row blocks over GPUs.  Here block b of
 * assembly: each rank assembles its rows (no communication -- panels,
   rules and the column tiling are replicated);
 * GMRES: every rank applies its row block to the replicated Krylov vector
-  and the block results are all-gathered (NCCL over NVLink; gloo in the CPU
-  tests) -- the only data-path collective.  Krylov basis, Hessenberg and
+  and the block results are all-gathered -- the only data-path exchange.
+  On the device path the GEMV's epilogue stores every row result straight
+  into all ranks' replicated vectors through CUDA-IPC-mapped peer memory
+  (PeerGather, csrc/peer.cu: NVLink stores + an epoch flag barrier); the
+  NCCL all-gather (RowGather) remains for the one-off row scans, for
+  HVB_PEER_GATHER=0, and when IPC is unavailable (gloo CPU tests).  Krylov basis, Hessenberg and
   Givens state are replicated and updated identically on every rank, so the
   solve needs no other communication and all ranks return the same u;
 * fields / tracing: targets split per rank, no communication.
@@ -17,11 +21,17 @@ PAPER.md:203 distributes the same row blocks over GPUs.  Here block b of
 
 from __future__ import annotations
 
+import logging
+import os
+
 import numpy as np
 
 from .assembly import DeviceStore, _rowmax_diag, assemble_rows, device_matvec, partition_rows
 
-__all__ = ["DistributedMatrix", "assemble_distributed", "RowGather", "split_range"]
+__all__ = ["DistributedMatrix", "assemble_distributed", "RowGather", "PeerGather", "split_range"]
+
+logger = logging.getLogger(__name__)
+LAST_GATHER = None  # "peer" or "nccl": the data-path exchange of the last distributed operator
 
 
 def split_range(total: int, world: int, rank: int):
@@ -66,16 +76,108 @@ class RowGather:
         return buf[self._idx[key]]
 
 
+class _CudaArray:
+    """Zero-copy torch view of raw device memory (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+
+
+class PeerGather:
+    """Fused GEMV + all-gather over CUDA IPC peer memory (csrc/peer.cu).
+
+    Every rank owns a cudaMalloc'd region -- two replicated N-vectors
+    (alternating by epoch parity) and a row of `world` epoch flags -- and
+    maps every peer's region.  One matvec = hvb_gemv_bcast (each row result
+    stored into all replicas over NVLink) + hvb_peer_signal + hvb_peer_wait;
+    no NCCL call and no separate gather launch on the data path."""
+
+    def __init__(self, total: int, group=None, device=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.total = total
+        self.device = device
+        h = _lib.lib()
+        vec_bytes = 8 * total
+        region = 2 * vec_bytes + 8 * self.world
+        base = ctypes.c_void_p()
+        _lib.call("hvb_ipc_alloc", region, ctypes.byref(base))
+        self._base = base.value
+        hb = h.hvb_ipc_handle_bytes()
+        handle = (ctypes.c_ubyte * hb)()
+        _lib.call("hvb_ipc_handle", ctypes.c_void_p(self._base), handle)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        bases, self._opened = [], []
+        for r, hd in enumerate(handles):
+            if r == self.rank:
+                bases.append(self._base)
+                continue
+            buf = (ctypes.c_ubyte * hb).from_buffer_copy(hd)
+            p = ctypes.c_void_p()
+            _lib.call("hvb_ipc_open", buf, ctypes.byref(p))
+            bases.append(p.value)
+            self._opened.append(p.value)
+        i64 = dict(dtype=torch.int64, device=device)
+        self.vec_ptrs = [torch.tensor([b + par * vec_bytes for b in bases], **i64) for par in (0, 1)]
+        self.flag_ptrs = torch.tensor([b + 2 * vec_bytes for b in bases], **i64)
+        self.my_flags = self._base + 2 * vec_bytes
+        self.local = [torch.as_tensor(_CudaArray(self._base + par * vec_bytes, total), device=device)
+                      for par in (0, 1)]
+        self.epoch = 0
+        dist.barrier(group=group)  # every peer has mapped every region
+
+    def matvec(self, store, row0: int, z, right, left_local):
+        """Full y = left .* A (z ./ right) from this rank's row block."""
+        from . import _lib
+        from .assembly import gather_operand
+
+        xp = gather_operand(store, z, right)
+        self.epoch += 1
+        par = self.epoch & 1
+        s = _lib.stream_ptr(self.device)
+        _lib.call("hvb_gemv_bcast", _lib.ptr(store.A), store.lda, int(store.A.shape[0]), store.size, _lib.ptr(xp),
+                  _lib.ptr(left_local), _lib.ptr(self.vec_ptrs[par]), self.world, row0, s)
+        _lib.call("hvb_peer_signal", _lib.ptr(self.flag_ptrs), self.world, self.rank, self.epoch, s)
+        _lib.call("hvb_peer_wait", __import__("ctypes").c_void_p(self.my_flags), self.world, self.epoch, s)
+        return self.local[par].clone()
+
+
+def _peer_gather_enabled() -> bool:
+    return os.environ.get("HVB_PEER_GATHER", "1") != "0"
+
+
 class _DistOperator:
     def __init__(self, dmat):
         self.dm = dmat
         self.device = dmat.device
         self.size = dmat.size
         self.gather = RowGather(dmat.size, dmat.group)
+        self.peer = None
+        st = dmat.store
+        if (_peer_gather_enabled() and st is not None and not st.is_f32 and dmat._apply is None
+                and self.device is not None and self.device.type == "cuda"):
+            try:
+                self.peer = PeerGather(dmat.size, dmat.group, self.device)
+            except Exception as exc:  # IPC unavailable: the NCCL all-gather path
+                logger.warning("peer-memory gather unavailable (%s); using the NCCL all-gather", exc)
+                self.peer = None
+        global LAST_GATHER
+        LAST_GATHER = "peer" if self.peer is not None else "collective"
 
     def apply(self, z, right=None, left=None):
         a, b = self.dm.start, self.dm.stop
         loc_left = None if left is None else left[a:b]
+        if self.peer is not None:
+            return self.peer.matvec(self.dm.store, a, z, right, loc_left)
         y = self.dm.local_apply(z, right, loc_left)
         return self.gather(y)
 

@@ -100,7 +100,9 @@ def _gpu_worker(rank, world, port, out_q):
         starts = np.array([[0.55, 0.0, 0.0], [0.0, 0.6, 0.0], [0.0, 0.0, -0.7]])
         la, lb = split_range(len(starts), world, rank)
         lines = trace_fieldlines(sol, m, starts[la:lb], [1] * (lb - la))
-        out_q.put((rank, sol.u, sol.iterations, E, [ln.points for ln in lines]))
+        from paper_2003_12663_b200 import parallel
+
+        out_q.put((rank, sol.u, sol.iterations, E, [ln.points for ln in lines], parallel.LAST_GATHER))
     finally:
         dist.destroy_process_group()
 
@@ -109,8 +111,9 @@ def _gpu_worker(rank, world, port, out_q):
 @pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
 def test_row_sharded_device_path_matches_single_process():
     """World-size 2 (gloo; both ranks on cuda:0) through the real device
-    path: row-block assembly, all-gathered GMRES, points and lines split
-    per rank -- bitwise the single-process results."""
+    path: row-block assembly, GMRES with the fused GEMV + peer-memory
+    all-gather (CUDA IPC), points and lines split per rank -- the
+    single-process results."""
     from paper_2003_12663_b200 import fixtures
     from paper_2003_12663_b200.assembly import assemble
     from paper_2003_12663_b200.postprocess import eval_efield_batch, trace_fieldlines
@@ -133,6 +136,7 @@ def test_row_sharded_device_path_matches_single_process():
     starts = np.array([[0.55, 0.0, 0.0], [0.0, 0.6, 0.0], [0.0, 0.0, -0.7]])
     lines = trace_fieldlines(sol, m, starts, [1, 1, 1])
     for r in res:
+        assert r[5] == "peer"  # fused GEMV + peer-memory all-gather (csrc/peer.cu)
         np.testing.assert_allclose(r[1], sol.u, rtol=0, atol=1e-13 * np.max(np.abs(sol.u)))
         assert abs(r[2] - sol.iterations) <= 1
     np.testing.assert_allclose(np.vstack([r[3] for r in res]), E, rtol=1e-12, atol=1e-14)
