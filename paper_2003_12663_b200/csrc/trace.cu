@@ -339,10 +339,30 @@ __global__ void __launch_bounds__(SD_THREADS) k_surface_distance(const double* _
     idx[k] = 0x7fffffff;
   }
   const int ng = (nt + 31) / 32;
+  // pass 1: T0 = min over full groups of ||x - C|| + rho_sd bounds the 12th
+  // smallest key from above (each such group holds 32 >= 12 panels whose
+  // keys are all <= it), so groups with ||x - C|| - rho_sd >= T0 (+ margin)
+  // cannot hold a top-12 panel
+  double t0 = INFINITY;
+  for (int g = tid; g < ng; g += SD_THREADS) {
+    if (32 * g + 32 > nt) continue;
+    const double* gb = groups + 8 * (size_t)g;
+    const double gd = __dsqrt_rn(sumsq_unfused(sub_rn(X, mk3(gb[0], gb[1], gb[2]))));
+    t0 = fmin(t0, (gd + gb[4]) * (1.0 + 1e-12));
+  }
+  s_key[tid] = t0;
+  __syncthreads();
+  for (int w = SD_THREADS / 2; w > 0; w >>= 1) {
+    if (tid < w) s_key[tid] = fmin(s_key[tid], s_key[tid + w]);
+    __syncthreads();
+  }
+  t0 = s_key[0];
+  __syncthreads();
   for (int g = tid; g < ng; g += SD_THREADS) {
     const double* gb = groups + 8 * (size_t)g;
     const double gd = __dsqrt_rn(sumsq_unfused(sub_rn(X, mk3(gb[0], gb[1], gb[2]))));
-    if (gd - gb[4] - 1e-12 * (gd + gb[4]) >= key[SD_K - 1]) continue;
+    const double glo = gd - gb[4] - 1e-12 * (gd + gb[4]);
+    if (glo >= key[SD_K - 1] || glo > t0) continue;
     const int tend = min(nt, 32 * g + 32);
   for (int t = 32 * g; t < tend; ++t) {
     const double* c = ccr + 4 * (size_t)t;
