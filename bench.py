@@ -366,7 +366,13 @@ def run_b200(args):
         rule), lines split per rank, device tracer + streamer verdicts."""
         if args.lines <= 0:
             return
-        se = postprocess.surface_field_magnitudes(mesh, sol)
+        if world > 1:  # each rank its share of the vertices, all-gathered (n doubles)
+            ia, ib = split_range(n, world, rank)
+            part = torch.as_tensor(postprocess.surface_field_magnitudes(mesh, sol, indices=np.arange(ia, ib)),
+                                   device=dev)
+            se = parallel.RowGather(n)(part).cpu().numpy()
+        else:
+            se = postprocess.surface_field_magnitudes(mesh, sol)
         starts, idx, _ = postprocess.pick_start_points(mesh, sol, args.lines, surface_e=se)
         la, lb = split_range(len(starts), world, rank)
         E0 = postprocess.eval_efield_batch(sol, mesh, starts[la:lb])

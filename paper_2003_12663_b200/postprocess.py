@@ -278,9 +278,10 @@ def eval_efield(solution, mesh: SurfaceMesh, x, cfg: QuadConfig | None = None) -
 
 
 def surface_field_magnitudes(mesh: SurfaceMesh, solution, cfg: QuadConfig | None = None, side: float = +1.0,
-                             workers: int = 1) -> np.ndarray:
+                             workers: int = 1, *, indices=None) -> np.ndarray:
     """|E| at every collocation point on the side the normal points into
-    (reference src/postprocess.py:141-170)."""
+    (reference src/postprocess.py:141-170).  ``indices`` (extension):
+    only these collocation points, in that order (a rank's share)."""
     import torch
 
     from .device import device_mesh
@@ -289,12 +290,20 @@ def surface_field_magnitudes(mesh: SurfaceMesh, solution, cfg: QuadConfig | None
     dm = device_mesh(mesh, cfg)
     u_dev, key = _u_device(solution, dm)
     src = _sources(dm, u_dev, key)
-    own = torch.arange(mesh.n_collocation, dtype=torch.int32, device=dm.device)
-    E = field_points_device(dm, u_dev, src, dm.points, False, own_col=own)
-    emag = torch.empty(mesh.n_collocation, dtype=torch.float64, device=dm.device)
+    if indices is None:
+        own = torch.arange(mesh.n_collocation, dtype=torch.int32, device=dm.device)
+        pts = dm.points
+    else:
+        own = torch.as_tensor(np.asarray(indices, dtype=np.int32), device=dm.device)
+        pts = dm.points[own.long()].contiguous()
+    m = int(own.shape[0])
+    if m == 0:
+        return np.zeros(0)
+    E = field_points_device(dm, u_dev, src, pts, False, own_col=own)
+    emag = torch.empty(m, dtype=torch.float64, device=dm.device)
     _lib.call("hvb_field_singular", _lib.ptr(dm.nodes6), _lib.ptr(dm.tri_cols), _lib.ptr(dm.vc_ptr),
               _lib.ptr(dm.vc_tri), _lib.ptr(dm.vc_corner), _lib.ptr(dm.rule_duffy), dm.n_duffy,
-              _lib.ptr(dm.points), _lib.ptr(dm.normals), _lib.ptr(own), mesh.n_collocation, _lib.ptr(u_dev),
+              _lib.ptr(pts), _lib.ptr(dm.normals), _lib.ptr(own), m, _lib.ptr(u_dev),
               float(side), _lib.ptr(E), _lib.ptr(emag), _lib.stream_ptr(dm.device))
     return emag.cpu().numpy()
 

@@ -99,3 +99,13 @@ def test_repeated_launches_bitwise(sphere):
     np.testing.assert_array_equal(eval_efield_batch(sol, m, P), eval_efield_batch(sol, m, P))
     # a point evaluated alone equals the same point inside a batch
     np.testing.assert_array_equal(eval_efield_batch(sol, m, P[100:101])[0], eval_efield_batch(sol, m, P)[100])
+
+
+def test_surface_field_subset_matches_full(sphere):
+    from paper_2003_12663_b200.postprocess import surface_field_magnitudes
+
+    m, _, _, sol = sphere
+    full = surface_field_magnitudes(m, sol)
+    idx = np.array([5, 0, 77, m.n_collocation - 1])
+    np.testing.assert_array_equal(surface_field_magnitudes(m, sol, indices=idx), full[idx])
+    assert surface_field_magnitudes(m, sol, indices=np.zeros(0, dtype=int)).shape == (0,)
