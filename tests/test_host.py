@@ -382,3 +382,22 @@ def test_line_state_layout_matches_library():
     lib = ctypes.CDLL(__graft_entry__.LIB)
     lib.hvb_line_state_bytes.restype = ctypes.c_int
     assert lib.hvb_line_state_bytes() == LINE_STATE_DTYPE.itemsize
+
+
+def test_public_api_mirrors_reference_init():
+    """Every name the reference package exports (src/__init__.py:8-64) is
+    importable from the drop-in package root."""
+    import paper_2003_12663_b200 as pkg
+
+    names = ["EPS0", "CurvedTriangle", "DielectricJump", "Dirichlet", "FloatingDirichlet", "MeshError", "PatchSpec",
+             "SurfaceMesh", "Vertex", "classify_vertex", "load_mesh", "map_reference", "parse_mesh", "save_mesh",
+             "surface_frame", "PairClass", "QuadConfig", "Rule", "classify_pair", "closest_point", "duffy_rule",
+             "near_singular_rule", "regular_rule", "subdivide_at", "SingularEvaluation", "adl_kernel",
+             "efield_kernel", "sl_kernel", "AssemblyError", "Neutrality", "SystemMatrix", "assemble", "charge_row",
+             "load_matrix", "matvec", "partition_rows", "save_matrix", "Solution", "SolverConfig", "SolverError",
+             "residual", "solve", "FieldLine", "IonizationModel", "TraceError", "TraceParams", "eval_efield",
+             "eval_potential", "load_ionization_model", "pick_start_points", "streamer_integral",
+             "surface_field_magnitudes", "trace_fieldline", "Config"]
+    missing = [n for n in names if not hasattr(pkg, n)]
+    assert not missing, missing
+    assert pkg.__version__ == "0.1.0"
