@@ -156,11 +156,11 @@ def _u_device(solution, dm):
     return hit[1], hit[0]
 
 
-PANELS_PER_SPLIT = 512
+PANELS_PER_SPLIT = int(__import__("os").environ.get("HVB_PANELS_PER_SPLIT", "256"))
 
 
 def panel_split(nt: int) -> int:
-    """Panel-range split of the N-body launch (grid.y): chunks of ~512
+    """Panel-range split of the N-body launch (grid.y): chunks of ~256
     panels.  A function of the mesh only, so every target's sum has the
     same order whatever the batch (results independent of batch size and
     GPU count), and small batches (the tracer's tail rounds) still spread
