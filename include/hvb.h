@@ -237,6 +237,8 @@ int hvb_bench_latency(double* out, int n, void* stream);
 int hvb_bench_nodes(double* out, int var, int blocks, int threads, int iters, void* stream);
 int hvb_bench_read(const double* p, long long n, double* out, int blocks, void* stream);
 int hvb_bench_rsqrt(const double* r2, int n, double* out, void* stream);
+int hvb_bench_gemv(const double* A, long long lda, int nrows, int ncols, const double* x, double* y, int variant,
+                   void* stream);
 
 #ifdef __cplusplus
 }

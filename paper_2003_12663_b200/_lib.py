@@ -58,6 +58,7 @@ SIGNATURES = {
     "hvb_bench_nodes": [_P, _I, _I, _I, _I, _P],
     "hvb_bench_read": [_P, _LL, _P, _I, _P],
     "hvb_bench_rsqrt": [_P, _I, _P, _P],
+    "hvb_bench_gemv": [_P, _LL, _I, _I, _P, _P, _I, _P],
 }
 
 HVB_EARG = 1

@@ -12,12 +12,20 @@
 // count, never on the row blocking: results are bitwise identical for any
 // block partition (reference invariance, tests/test_assembly.py:72-78).
 #include <cooperative_groups.h>
+#include <cstdint>
 
 #include "launch.cuh"
 
 namespace hvb {
 
 constexpr int GEMV_THREADS = 256;
+
+// 256-bit non-allocating global load of 4 doubles (LDG.E.NA.ENL2.256)
+HVB_DEV void ld256(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
 
 // outs != nullptr: the fused all-gather -- each row result is stored into
 // all n_out replicated vectors (this GPU's and every peer's, mapped over
@@ -150,7 +158,18 @@ __global__ void k_rowmax_diag(const T* A, int64_t lda, int nrows, int ncols, con
   if (r >= nrows) return;
   const T* row = A + (int64_t)r * lda;
   double m = 0.0;
-  for (int k = threadIdx.x; k < ncols; k += blockDim.x) m = fmax(m, fabs((double)row[k]));
+  if (sizeof(T) == 8 && lda % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 31) == 0) {
+    const double* rd = reinterpret_cast<const double*>(row);
+    const int n4 = ncols >> 2;
+    for (int k = threadIdx.x; k < n4; k += blockDim.x) {
+      double a, b, c, d;
+      ld256(rd + 4 * k, a, b, c, d);
+      m = fmax(m, fmax(fmax(fabs(a), fabs(b)), fmax(fabs(c), fabs(d))));
+    }
+    for (int k = 4 * n4 + threadIdx.x; k < ncols; k += blockDim.x) m = fmax(m, fabs(rd[k]));
+  } else {
+    for (int k = threadIdx.x; k < ncols; k += blockDim.x) m = fmax(m, fabs((double)row[k]));
+  }
   __shared__ double red[32];
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
@@ -163,24 +182,46 @@ __global__ void k_rowmax_diag(const T* A, int64_t lda, int nrows, int ncols, con
   }
 }
 
+template <int ROWS>
+__global__ void k_gemv_f64_v4(const double* __restrict__ A, int64_t lda, int nrows, int ncols,
+                              const double* __restrict__ x, const double* __restrict__ left, double* __restrict__ y,
+                              double* const* outs, int n_out, int64_t out_off);
+
+// 256-bit loads need 32-byte aligned rows and x: the production FP64 path
+// (2 rows per CTA, LDG.256 non-allocating: 7.5 TB/s on a cfg4-width block vs
+// 5.7 TB/s for 128-bit loads and 8 rows per CTA, tools/gemv_probe.py)
+static bool v4_ok(const void* A, int64_t lda, const double* x) {
+  return lda % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 31) == 0 && (reinterpret_cast<uintptr_t>(x) & 31) == 0;
+}
+
 cudaError_t launch_gemv(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const double* x,
                         const double* left, double* y, cudaStream_t st) {
   if (nrows == 0) return cudaSuccess;
-  constexpr int R = 8;
-  dim3 grid((nrows + R - 1) / R);
-  if (is_f32)
-    k_gemv_f32<R><<<grid, GEMV_THREADS, 0, st>>>((const float*)A, lda, nrows, ncols, x, left, y);
-  else
-    k_gemv_f64<R><<<grid, GEMV_THREADS, 0, st>>>((const double*)A, lda, nrows, ncols, x, left, y, nullptr, 0, 0);
+  if (is_f32) {
+    constexpr int R = 8;
+    k_gemv_f32<R><<<(nrows + R - 1) / R, GEMV_THREADS, 0, st>>>((const float*)A, lda, nrows, ncols, x, left, y);
+  } else if (v4_ok(A, lda, x)) {
+    k_gemv_f64_v4<2><<<(nrows + 1) / 2, GEMV_THREADS, 0, st>>>((const double*)A, lda, nrows, ncols, x, left, y,
+                                                               nullptr, 0, 0);
+  } else {
+    constexpr int R = 4;
+    k_gemv_f64<R><<<(nrows + R - 1) / R, GEMV_THREADS, 0, st>>>((const double*)A, lda, nrows, ncols, x, left, y,
+                                                                nullptr, 0, 0);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemv_bcast(const double* A, int64_t lda, int nrows, int ncols, const double* x, const double* left,
                               double* const* outs, int n_out, int64_t out_off, cudaStream_t st) {
   if (nrows == 0) return cudaSuccess;
-  constexpr int R = 8;
-  dim3 grid((nrows + R - 1) / R);
-  k_gemv_f64<R><<<grid, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, left, nullptr, outs, n_out, out_off);
+  if (v4_ok(A, lda, x)) {
+    k_gemv_f64_v4<2><<<(nrows + 1) / 2, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, left, nullptr, outs, n_out,
+                                                               out_off);
+  } else {
+    constexpr int R = 4;
+    k_gemv_f64<R><<<(nrows + R - 1) / R, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, left, nullptr, outs, n_out,
+                                                                out_off);
+  }
   return cudaGetLastError();
 }
 
@@ -298,3 +339,86 @@ cudaError_t launch_mgs(const double* V, long long ldv, int j, double* w, int n, 
 }
 
 }  // namespace hvb
+
+// ---------------------------------------------------------------------------
+// 256-bit-load GEMV variant (LDG.E.NA.ENL2.256: 4 doubles per load, no L1
+// allocation): same per-row summation structure as k_gemv_f64 over 4-column
+// chunks.  Used by hvb_gemv when lda % 4 == 0 (A/B in tools/gemv_probe.py).
+// ---------------------------------------------------------------------------
+namespace hvb {
+
+
+template <int ROWS>
+__global__ void k_gemv_f64_v4(const double* __restrict__ A, int64_t lda, int nrows,
+                                                              int ncols, const double* __restrict__ x,
+                                                              const double* __restrict__ left,
+                                                              double* __restrict__ y, double* const* outs, int n_out,
+                                                              int64_t out_off) {
+  const int r0 = blockIdx.x * ROWS;
+  const int tid = threadIdx.x;
+  double acc[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) acc[r] = 0.0;
+  const int n4 = ncols >> 2;
+  const double* rowp[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) rowp[r] = A + (int64_t)min(r0 + r, nrows - 1) * lda;
+#pragma unroll 2
+  for (int k = tid; k < n4; k += GEMV_THREADS) {
+    const double4 xv = *reinterpret_cast<const double4*>(x + 4 * k);
+    double a[ROWS][4];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) ld256(rowp[r] + 4 * k, a[r][0], a[r][1], a[r][2], a[r][3]);
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+      acc[r] = fma(a[r][3], xv.w, fma(a[r][2], xv.z, fma(a[r][1], xv.y, fma(a[r][0], xv.x, acc[r]))));
+  }
+  if (tid == 0) {
+    for (int c = 4 * n4; c < ncols; ++c) {
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) acc[r] = fma(rowp[r][c], x[c], acc[r]);
+    }
+  }
+  __shared__ double red[ROWS][GEMV_THREADS / 32];
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    double v = warp_sum(acc[r]);
+    if (lane == 0) red[r][wid] = v;
+  }
+  __syncthreads();
+  if (tid < ROWS && r0 + tid < nrows) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < GEMV_THREADS / 32; ++w) s += red[tid][w];
+    const double v = left ? left[r0 + tid] * s : s;
+    if (outs) {
+      for (int k = 0; k < n_out; ++k) outs[k][out_off + r0 + tid] = v;
+    } else {
+      y[r0 + tid] = v;
+    }
+  }
+}
+
+cudaError_t launch_gemv_variant(const double* A, int64_t lda, int nrows, int ncols, const double* x, double* y,
+                                int variant, cudaStream_t st) {
+  switch (variant) {
+    case 0: k_gemv_f64<8><<<(nrows + 7) / 8, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
+    case 1: k_gemv_f64_v4<8><<<(nrows + 7) / 8, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
+    case 2: k_gemv_f64_v4<4><<<(nrows + 3) / 4, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
+    case 3: k_gemv_f64_v4<16><<<(nrows + 15) / 16, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
+    case 4: k_gemv_f64<4><<<(nrows + 3) / 4, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
+    case 5: k_gemv_f64<16><<<(nrows + 15) / 16, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
+    case 6: k_gemv_f64_v4<2><<<(nrows + 1) / 2, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
+    case 7: k_gemv_f64_v4<1><<<nrows, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hvb
+
+extern "C" int hvb_bench_gemv(const double* A, long long lda, int nrows, int ncols, const double* x, double* y,
+                              int variant, void* stream) {
+  return hvb::launch_gemv_variant(A, lda, nrows, ncols, x, y, variant, (cudaStream_t)stream) == cudaSuccess ? 0 : 2;
+}

@@ -20,6 +20,20 @@ __global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, doubl
   if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 
+// read-only HBM stream with 256-bit non-allocating loads (the GEMV's load)
+__global__ void __launch_bounds__(256) k_read_stream4(const double* __restrict__ p, long long n4, double* out) {
+  double acc = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    double a, b, c, d;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+                 : "l"(p + 4 * i));
+    acc += (a + b) + (c + d);
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
 __global__ void __launch_bounds__(256) k_read_stream(const double2* __restrict__ p, long long n2, double* out) {
   double acc = 0.0;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -169,6 +183,9 @@ extern "C" int hvb_bench_dfma(double* out, int blocks, int iters, void* stream) 
 }
 
 extern "C" int hvb_bench_read(const double* p, long long n, double* out, int blocks, void* stream) {
-  hvb::k_read_stream<<<blocks, 256, 0, (cudaStream_t)stream>>>((const double2*)p, n / 2, out);
+  if (n % 4 == 0)
+    hvb::k_read_stream4<<<blocks, 256, 0, (cudaStream_t)stream>>>(p, n / 4, out);
+  else
+    hvb::k_read_stream<<<blocks, 256, 0, (cudaStream_t)stream>>>((const double2*)p, n / 2, out);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
