@@ -53,7 +53,8 @@ int hvb_build_stream(const double* table, int nq, const double* ccr, double eta,
  * near_list as (row-list index, triangle).  mode: 0 all-SL, 1 all-ADL,
  * 2 mixed; | W << 8 = W-column window (row4: 40, 48, 56, 64), else | 4 =
  * 64-column window, else 96; | R << 16 = R records per lane (row layouts:
- * 2, 3, 4 or 8; the stream band is bounded over groups of R). | 8 = quad layout (the panel
+ * 4 or 8; the stream band is bounded over groups of R); | 1 << 20 = row
+ * layouts flush 16 columns at a time (band <= window - 16, else - 32). | 8 = quad layout (the panel
  * stream's band is bounded over groups of 4 records, else 2); | 16 = row4
  * layout (lane = row, 4 records per lane; same stream as quad); | 32 = row8
  * (8 records per lane, band over groups of 8).

@@ -34,7 +34,7 @@ HVB_DEV bool regular(double sq, const double* cg) {
 }
 }  // namespace row4
 
-template <int NQ, int MODE, int WIN, int R>
+template <int NQ, int MODE, int WIN, int R, int FLUSH>
 __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
   using namespace row4;
   constexpr int REC = 6 * NQ + 8;
@@ -84,16 +84,32 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
   commit();
 
   int base = 0;
-  auto flush32 = [&](int b) {
-    const int c = b + lane;
+  // flush FLUSH finished columns: FLUSH = 16 -- lanes 0-15 write rows 0-15
+  // and lanes 16-31 rows 16-31 of 16 consecutive columns (128-byte row
+  // segments) -- so the window only needs band + 16 columns: a 48-column
+  // window holds the band-32 tiling (1.14 redundancy)
+  auto flush = [&](int b) {
+    const int c = b + (FLUSH == 16 ? (lane & 15) : lane);
     double* wcol = win + (c % WIN) * STRIDE;
     const bool in = c < width;
+    if (FLUSH == 16) {
+      const int rh = (lane >> 4) * 16;
 #pragma unroll 8
-    for (int j = 0; j < ROWS; ++j) {
-      const int64_t off = __shfl_sync(0xffffffffu, fout, j);
-      const double sc = __shfl_sync(0xffffffffu, fscale, j);
-      if (off >= 0 && in) a.A[off + col0 + c] = wcol[j] * sc;
-      wcol[j] = 0.0;
+      for (int j = 0; j < 16; ++j) {
+        const int row = rh + j;
+        const int64_t off = __shfl_sync(0xffffffffu, fout, row);
+        const double sc = __shfl_sync(0xffffffffu, fscale, row);
+        if (off >= 0 && in) a.A[off + col0 + c] = wcol[row] * sc;
+        wcol[row] = 0.0;
+      }
+    } else {
+#pragma unroll 8
+      for (int j = 0; j < ROWS; ++j) {
+        const int64_t off = __shfl_sync(0xffffffffu, fout, j);
+        const double sc = __shfl_sync(0xffffffffu, fscale, j);
+        if (off >= 0 && in) a.A[off + col0 + c] = wcol[j] * sc;
+        wcol[j] = 0.0;
+      }
     }
     __syncwarp();
   };
@@ -105,9 +121,9 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
     __syncwarp();
     const double* pr = ring + (p & 1) * SREC;
     const int mfirst = reinterpret_cast<const int*>(pr + 6 * NQ + 6)[1];
-    while (mfirst >= base + 32) {
-      flush32(base);
-      base += 32;
+    while (mfirst >= base + FLUSH) {
+      flush(base);
+      base += FLUSH;
     }
     double acc[R][3];
 #pragma unroll
@@ -196,8 +212,8 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
   wait_group<0>();
   __syncwarp();
   while (base < width) {
-    flush32(base);
-    base += 32;
+    flush(base);
+    base += FLUSH;
   }
 }
 
@@ -206,7 +222,7 @@ static size_t row4_smem_bytes(int nq, int r) {
   return (size_t)(row4::Shape<WIN>::WREG + row4::DEPTH * r * (6 * nq + 8)) * sizeof(double);
 }
 
-template <int NQ, int WIN, int R>
+template <int NQ, int WIN, int R, int FLUSH>
 static cudaError_t launch_row4_nq(const RegularArgs& a, int mode, cudaStream_t st) {
   dim3 grid((a.n_rows + row4::ROWS - 1) / row4::ROWS, a.n_tiles);
   const size_t smem = row4_smem_bytes<WIN>(NQ, R);
@@ -215,35 +231,37 @@ static cudaError_t launch_row4_nq(const RegularArgs& a, int mode, cudaStream_t s
     kern<<<grid, 32, smem, st>>>(a);
     return cudaGetLastError();
   };
-  if (mode == 0) return go(k_assemble_row4<NQ, 0, WIN, R>);
-  if (mode == 1) return go(k_assemble_row4<NQ, 1, WIN, R>);
-  return go(k_assemble_row4<NQ, 2, WIN, R>);
+  if (mode == 0) return go(k_assemble_row4<NQ, 0, WIN, R, FLUSH>);
+  if (mode == 1) return go(k_assemble_row4<NQ, 1, WIN, R, FLUSH>);
+  return go(k_assemble_row4<NQ, 2, WIN, R, FLUSH>);
 }
 
-// window 64 (band over groups of R records <= 32) or 96 (groups of 4, <= 64);
-// R = 4 or 8 records per lane per step
-cudaError_t launch_regular_row4(const RegularArgs& a, int nq, int mode, int window, int r, cudaStream_t st) {
-  auto pick = [&](auto win_tag, auto r_tag) -> cudaError_t {
+// window WIN, R records per lane per step, flush width 16 or 32: the
+// stream's band (over groups of R records) must be <= WIN - flush
+cudaError_t launch_regular_row4(const RegularArgs& a, int nq, int mode, int window, int r, int flush,
+                                cudaStream_t st) {
+  auto pick = [&](auto win_tag, auto r_tag, auto f_tag) -> cudaError_t {
     constexpr int W = decltype(win_tag)::value;
     constexpr int RR = decltype(r_tag)::value;
+    constexpr int F = decltype(f_tag)::value;
     switch (nq) {
-      case 3: return launch_row4_nq<3, W, RR>(a, mode, st);
-      case 6: return launch_row4_nq<6, W, RR>(a, mode, st);
-      case 12: return launch_row4_nq<12, W, RR>(a, mode, st);
-      case 16: return launch_row4_nq<16, W, RR>(a, mode, st);
+      case 3: return launch_row4_nq<3, W, RR, F>(a, mode, st);
+      case 6: return launch_row4_nq<6, W, RR, F>(a, mode, st);
+      case 12: return launch_row4_nq<12, W, RR, F>(a, mode, st);
+      case 16: return launch_row4_nq<16, W, RR, F>(a, mode, st);
     }
     return cudaErrorInvalidValue;
   };
   using I4 = std::integral_constant<int, 4>;
-  using I8 = std::integral_constant<int, 8>;
-  if (window == 48 && r == 4) return pick(std::integral_constant<int, 48>{}, I4{});
-  if (window == 48 && r == 2) return pick(std::integral_constant<int, 48>{}, std::integral_constant<int, 2>{});
-  if (window == 48 && r == 3) return pick(std::integral_constant<int, 48>{}, std::integral_constant<int, 3>{});
-  if (window == 40 && r == 4) return pick(std::integral_constant<int, 40>{}, I4{});
-  if (window == 56 && r == 4) return pick(std::integral_constant<int, 56>{}, I4{});
-  if (window == 64 && r == 8) return pick(std::integral_constant<int, 64>{}, I8{});
-  if (window == 64 && r == 4) return pick(std::integral_constant<int, 64>{}, I4{});
-  if (window == 96 && r == 4) return pick(std::integral_constant<int, 96>{}, I4{});
+  using F16 = std::integral_constant<int, 16>;
+  using F32 = std::integral_constant<int, 32>;
+  if (window == 48 && r == 4 && flush == 16) return pick(std::integral_constant<int, 48>{}, I4{}, F16{});
+  if (window == 40 && r == 4 && flush == 16) return pick(std::integral_constant<int, 40>{}, I4{}, F16{});
+  if (window == 44 && r == 4 && flush == 16) return pick(std::integral_constant<int, 44>{}, I4{}, F16{});
+  if (window == 56 && r == 4 && flush == 16) return pick(std::integral_constant<int, 56>{}, I4{}, F16{});
+  if (window == 48 && r == 4 && flush == 32) return pick(std::integral_constant<int, 48>{}, I4{}, F32{});
+  if (window == 64 && r == 4 && flush == 32) return pick(std::integral_constant<int, 64>{}, I4{}, F32{});
+  if (window == 64 && r == 8 && flush == 32) return pick(std::integral_constant<int, 64>{}, std::integral_constant<int, 8>{}, F32{});
   return cudaErrorInvalidValue;
 }
 

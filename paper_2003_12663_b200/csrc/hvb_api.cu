@@ -55,7 +55,8 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
   if (n_rows <= 0 || n_tiles <= 0) return HVB_OK;
   // window columns: bits 8-15 if set (row4: 40/48/56/64), else bit 2 -> 64, else 96
   const int window = ((mode >> 8) & 0xff) ? (mode >> 8) & 0xff : (mode & 4) ? 64 : 96;
-  const int rpl = (mode >> 16) & 0xf;  // row layouts: records per lane per step (bits 16-19; 0 = layout default)
+  const int rpl = (mode >> 16) & 0xf;
+  const bool flush16 = (mode >> 20) & 1;  // bit 20: row layouts flush 16 columns at a time (band <= window - 16)  // row layouts: records per lane per step (bits 16-19; 0 = layout default)
   const bool quad = (mode & 8) != 0;        // bit 3: quad layout (tiling band over groups of 4 records)
   const bool row4 = (mode & 16) != 0;       // bit 4: row4 layout (same tiling as quad)
   const bool row8 = (mode & 32) != 0;       // bit 5: row8 layout (band over groups of 8 records)
@@ -82,7 +83,8 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
   a.near_count = near_count;
   a.near_cap = near_cap;
   if (row4 || row8)
-    return check(hvb::launch_regular_row4(a, nq, mode, window, (rpl ? rpl : row8 ? 8 : 4), (cudaStream_t)stream),
+    return check(hvb::launch_regular_row4(a, nq, mode, window, (rpl ? rpl : row8 ? 8 : 4), flush16 ? 16 : 32,
+                                          (cudaStream_t)stream),
                  "hvb_assemble_regular");
   if (quad)
     return check(hvb::launch_regular_quad(a, nq, mode, window, (cudaStream_t)stream), "hvb_assemble_regular");

@@ -84,7 +84,8 @@ struct FieldArgs {
 
 cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, int window, int wpb, cudaStream_t st);
 cudaError_t launch_regular_quad(const RegularArgs& a, int nq, int mode, int window, cudaStream_t st);
-cudaError_t launch_regular_row4(const RegularArgs& a, int nq, int mode, int window, int r, cudaStream_t st);
+cudaError_t launch_regular_row4(const RegularArgs& a, int nq, int mode, int window, int r, int flush,
+                                cudaStream_t st);
 cudaError_t launch_build_table(const double* nodes6, int nt, int nq, const double* rule, double* out,
                                cudaStream_t st);
 cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,

@@ -46,6 +46,11 @@ RPL = int(__import__("os").environ.get("HVB_ASM_R", "0"))  # row layouts: record
 GROUP = RPL if RPL and LAYOUT == "row4" else {"dual": 2, "quad": 4, "row4": 4, "row8": 8}[LAYOUT]
 LAYOUT_BITS = {"dual": 0, "quad": 8, "row4": 16, "row8": 32}[LAYOUT] | ((RPL << 16) if LAYOUT == "row4" else 0)
 WINDOW = WINDOW or (48 if LAYOUT == "row4" else 64)
+# row4 flushes 16 finished columns at a time, so a WINDOW-column window holds
+# a band of WINDOW - 16 (else WINDOW - 32)
+FLUSH = int(__import__("os").environ.get("HVB_ASM_FLUSH", "16")) if LAYOUT == "row4" else 32
+if FLUSH == 16:
+    LAYOUT_BITS |= 1 << 20
 # circumcentre-centred panel records (csrc/tables.cu, centered = 1) save two
 # FP64 ops per node-row but need 8 doubles per node: the bigger ring drops
 # row4 to 9 resident warps/SM and it measured slower (0.365 vs 0.343 s on
@@ -241,7 +246,7 @@ class DeviceMesh:
 
         # column tiling + panel streams
         self.window = WINDOW
-        tiling = mesh_tiling(mesh, max_tile, WINDOW, STRIPS, GROUP)
+        tiling = mesh_tiling(mesh, max_tile, WINDOW, STRIPS, GROUP, FLUSH)
         self.layout_bits = LAYOUT_BITS
         self.tiling = tiling
         self.perm = torch.as_tensor(tiling.perm, **i32)
@@ -289,13 +294,14 @@ def panel_groups(cc: np.ndarray, radii: np.ndarray, thr: np.ndarray) -> np.ndarr
     return out
 
 
-def mesh_tiling(mesh, max_tile: int = 2048, window: int = 96, strips: bool = False, group: int = 2) -> ColumnTiling:
+def mesh_tiling(mesh, max_tile: int = 2048, window: int = 96, strips: bool = False, group: int = 2,
+                flush: int = 32) -> ColumnTiling:
     """Host column tiling of a mesh (a mesh-derived array, cached on it)."""
-    key = ("tiling", max_tile, window, strips, group)
+    key = ("tiling", max_tile, window, strips, group, flush)
     cache = mesh._device_cache
     t = cache.get(key)
     if t is None:
-        t = column_tiling(mesh.colloc_points, mesh.tri_corner_cols, max_tile=max_tile, band_max=window - 32,
+        t = column_tiling(mesh.colloc_points, mesh.tri_corner_cols, max_tile=max_tile, band_max=window - flush,
                           group=group, strips=strips)
         cache[key] = t
     return t

@@ -209,6 +209,7 @@ def test_regular_sweep_layouts(cases, monkeypatch):
     m._device_cache.clear()
     monkeypatch.setattr(device, "LAYOUT_BITS", 8)
     monkeypatch.setattr(device, "WINDOW", 64)
+    monkeypatch.setattr(device, "FLUSH", 32)
     monkeypatch.setattr(device, "CENTERED", False)
     monkeypatch.setattr(device, "GROUP", 4)
     b = assemble(m)[0].toarray()
