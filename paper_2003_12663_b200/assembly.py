@@ -22,6 +22,7 @@ floating columns.
 
 from __future__ import annotations
 
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -346,7 +347,7 @@ def _span(label, e0):
 
 # warps per CTA of the regular sweep (csrc/assemble_dual.cu; ~29 KB of
 # shared memory per warp -> 7 resident warps per SM with 1-warp CTAs)
-_WPB = int(__import__("os").environ.get("HVB_ASM_WPB", "1"))
+_WPB = int(os.environ.get("HVB_ASM_WPB", "1"))
 
 
 def _run_rows(dm, plan: RowPlan, A, counts: dict, warps_per_block: int = 4):

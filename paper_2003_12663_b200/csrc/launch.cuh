@@ -125,7 +125,7 @@ cudaError_t launch_field_singular(const double* nodes6, const int* tri_cols, con
                                   double* efield, double* emag, cudaStream_t st);
 
 // ---- device tracer (trace.cu) ----
-constexpr int kPhaseStart = 0, kPhaseSD = 1, kPhaseStage = 2, kPhaseAccept = 3, kPhaseSnap = 4, kPhaseDone = 5;
+constexpr int kPhaseStart = 0, kPhaseSD = 1, kPhaseStage = 2, kPhaseSnap = 4, kPhaseDone = 5;  // 3: unused
 constexpr int kSurfaceHit = 0, kWeakField = 1, kMaxLength = 2, kLeftDomain = 3;
 constexpr int kStatusRunning = 0, kStatusDone = 1, kStatusWeakStart = 2, kStatusCoincident = 3;
 

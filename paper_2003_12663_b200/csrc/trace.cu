@@ -249,22 +249,6 @@ __global__ void k_trace_ctrl(TraceArgs a, int mode) {
       loop_body(a, L, line);  // x unchanged: the cached surface distance holds
       break;
     }
-    case kPhaseAccept: {
-      if (coincident) {
-        finish(a, L, L.term, kStatusCoincident);
-        break;
-      }
-      const bool ok = tangent(a, L, e, t, mag);
-      append(a, L, line, L.x, mag, L.s);
-      if (!ok) {
-        finish(a, L, kWeakField, kStatusDone);
-        break;
-      }
-      for (int d = 0; d < 3; ++d) L.k[0][d] = t[d];
-      step_size(a, L);
-      request_sd(a, L, line);
-      break;
-    }
     case kPhaseSnap: {
       if (!coincident) a.out_pts[((size_t)line * a.cap + (L.npts - 1)) * 5 + 3] = norm3(e);
       finish(a, L, kSurfaceHit, kStatusDone);

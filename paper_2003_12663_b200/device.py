@@ -4,13 +4,17 @@ Host side (NumPy, once per mesh):
 
 * ``column_tiling`` -- the matrix is stored in a *device column order*:
   recursive coordinate bisection of the collocation points into compact
-  tiles of at most ``max_tile`` columns, each tile swept along its longest
-  axis.  A panel that touches a tile contributes to its *owned* corners
-  only; within a tile the owned corners of any panel lie within ``band``
-  columns of its first owned corner, which is what lets the assembly kernel
-  keep a 96-column sliding window per warp (csrc/assemble.cu).  Panels with
-  corners in several tiles are evaluated once per tile (``redundancy``).
+  column tiles, each swept along its longest axis.  A panel that touches a
+  tile contributes to its *owned* corners only; within a tile the owned
+  corners of every aligned group of GROUP consecutive records lie within
+  ``band`` columns of the group's first owned column, which is what lets
+  the assembly warp keep a WINDOW-column sliding window of running sums
+  (csrc/assemble_row4.cu: WINDOW 48, flushes of 16 columns, band 32).
+  Panels with corners in several tiles are evaluated once per tile
+  (``redundancy``, 1.14 at config 4).
 * entries (tile, panel) sorted by (tile, first owned column).
+* ``panel_groups`` -- bounds of aligned 32-panel groups for the N-body and
+  surface-distance kernels.
 
 Device side (``DeviceMesh``, cached per device/config): panel nodes,
 circumcircles, sample tables (K1), the packed panel streams, rule tables
@@ -19,6 +23,7 @@ circumcircles, sample tables (K1), the packed panel streams, rule tables
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -28,27 +33,27 @@ from .quadrature import QuadConfig, duffy_rule, graded_rule, regular_rule
 
 __all__ = ["ColumnTiling", "column_tiling", "DeviceMesh", "device_mesh", "WINDOW_BAND"]
 
-WINDOW_BAND = 64  # csrc/assemble_dual.cu: WIN - 32 for the default 96-column window
+WINDOW_BAND = 64  # default band of column_tiling (dual layout, 96-column window)
 # regular-sweep window (row4: 40/48/56/64 columns, dual/quad: 64/96) and tile
 # shape; env overrides are for A/B measurements (tools/ab.sh).  Measured on
 # cfg4 (regular kernel): row4 x 48 columns 0.319 s, x 56 0.336, x 64 0.346,
 # x 40 0.360 (the window's shared memory sets the resident warps; a narrower
 # window means more tile-boundary panels: redundancy 1.14 at 64, 1.21 at 48)
-WINDOW = int(__import__("os").environ.get("HVB_ASM_WIN", "0"))  # 0: 48 for row4 (best on cfg4), else 64
-STRIPS = __import__("os").environ.get("HVB_ASM_STRIPS", "1") == "1"
+WINDOW = int(os.environ.get("HVB_ASM_WIN", "0"))  # 0: 48 for row4 (best on cfg4), else 64
+STRIPS = os.environ.get("HVB_ASM_STRIPS", "1") == "1"
 # quad layout (csrc/assemble_quad.cu: 2 records x 2 rows per lane) needs the
 # band bounded over groups of 4 records; the dual layout over groups of 2
 # row4 layout (csrc/assemble_row4.cu: lane = row, 4 records per lane) uses
 # the same stream as quad
-LAYOUT = __import__("os").environ.get("HVB_ASM_LAYOUT", "row4")
+LAYOUT = os.environ.get("HVB_ASM_LAYOUT", "row4")
 QUAD = LAYOUT in ("quad", "row4", "row8")
-RPL = int(__import__("os").environ.get("HVB_ASM_R", "0"))  # row layouts: records per lane (0 = default)
+RPL = int(os.environ.get("HVB_ASM_R", "0"))  # row layouts: records per lane (0 = default)
 GROUP = RPL if RPL and LAYOUT == "row4" else {"dual": 2, "quad": 4, "row4": 4, "row8": 8}[LAYOUT]
 LAYOUT_BITS = {"dual": 0, "quad": 8, "row4": 16, "row8": 32}[LAYOUT] | ((RPL << 16) if LAYOUT == "row4" else 0)
 WINDOW = WINDOW or (48 if LAYOUT == "row4" else 64)
 # row4 flushes 16 finished columns at a time, so a WINDOW-column window holds
 # a band of WINDOW - 16 (else WINDOW - 32)
-FLUSH = int(__import__("os").environ.get("HVB_ASM_FLUSH", "16")) if LAYOUT == "row4" else 32
+FLUSH = int(os.environ.get("HVB_ASM_FLUSH", "16")) if LAYOUT == "row4" else 32
 if FLUSH == 16:
     LAYOUT_BITS |= 1 << 20
 # circumcentre-centred panel records (csrc/tables.cu, centered = 1) save two
@@ -56,7 +61,7 @@ if FLUSH == 16:
 # row4 to 9 resident warps/SM and it measured slower (0.365 vs 0.343 s on
 # cfg4), so every layout reads the plain 6-double records
 CENTERED = False
-MAX_TILE = int(__import__("os").environ.get("HVB_ASM_MAXTILE", "32767"))
+MAX_TILE = int(os.environ.get("HVB_ASM_MAXTILE", "32767"))
 
 
 @dataclass

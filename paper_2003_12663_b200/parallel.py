@@ -137,6 +137,8 @@ class PeerGather:
 
     def matvec(self, store, row0: int, z, right, left_local):
         """Full y = left .* A (z ./ right) from this rank's row block."""
+        import ctypes
+
         from . import _lib
         from .assembly import gather_operand
 
@@ -147,7 +149,7 @@ class PeerGather:
         _lib.call("hvb_gemv_bcast", _lib.ptr(store.A), store.lda, int(store.A.shape[0]), store.size, _lib.ptr(xp),
                   _lib.ptr(left_local), _lib.ptr(self.vec_ptrs[par]), self.world, row0, s)
         _lib.call("hvb_peer_signal", _lib.ptr(self.flag_ptrs), self.world, self.rank, self.epoch, s)
-        _lib.call("hvb_peer_wait", __import__("ctypes").c_void_p(self.my_flags), self.world, self.epoch, s)
+        _lib.call("hvb_peer_wait", ctypes.c_void_p(self.my_flags), self.world, self.epoch, s)
         return self.local[par].clone()
 
 

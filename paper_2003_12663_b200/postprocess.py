@@ -11,6 +11,7 @@ are thin wrappers with identical results.
 
 from __future__ import annotations
 
+import os
 import csv
 from dataclasses import dataclass
 
@@ -156,7 +157,7 @@ def _u_device(solution, dm):
     return hit[1], hit[0]
 
 
-PANELS_PER_SPLIT = int(__import__("os").environ.get("HVB_PANELS_PER_SPLIT", "256"))
+PANELS_PER_SPLIT = int(os.environ.get("HVB_PANELS_PER_SPLIT", "256"))
 
 
 def panel_split(nt: int) -> int:
