@@ -5,6 +5,8 @@
 // row instead of two (twice the shared-memory broadcast loads).  Same
 // record stream, tiling guarantee (groups of 4), classification and
 // summation order as the quad layout.
+#include <cstdlib>
+
 #include "launch.cuh"
 
 namespace hvb {
@@ -34,8 +36,8 @@ HVB_DEV bool regular(double sq, const double* cg) {
 }
 }  // namespace row4
 
-template <int NQ, int MODE, int WIN, int R, int FLUSH>
-__global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
+template <int NQ, int MODE, int WIN, int R, int FLUSH, int WPC>
+__global__ void __launch_bounds__(32 * WPC) k_assemble_row4(RegularArgs a) {
   using namespace row4;
   constexpr int REC = 6 * NQ + 8;
   constexpr int SREC = R * REC;
@@ -43,13 +45,17 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
   constexpr int WREG = Shape<WIN>::WREG;
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
-  double* win = smem;
-  double* ring = win + WREG;
+  const int wib = threadIdx.x >> 5;
+  // WPC warps of the CTA take consecutive 32-row tiles of the SAME column
+  // tile and share one record ring (staged by all threads, CTA barriers),
+  // so the per-warp shared memory is the window plus 1/WPC of the ring
+  double* ring = smem;
+  double* win = smem + DEPTH * SREC + wib * WREG;
 
-  const int rowtile = blockIdx.x;
+  const int rowtile = blockIdx.x * WPC + wib;
   const int tile = blockIdx.y;
   const int base_row = rowtile * ROWS;
-  if (base_row >= a.n_rows) return;
+  if (WPC == 1 && base_row >= a.n_rows) return;  // (WPC > 1: warps past the end stay for the barriers)
 
   const int i0 = base_row + lane;
   const bool live0 = i0 < a.n_rows;
@@ -78,7 +84,7 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
     const double* s = src + (size_t)(R * p) * REC;
     const int nrec = min(R, ne - R * p);
     const int nch = nrec * (REC / 2);
-    for (int c = lane; c < nch; c += 32) cp_async16(dst + 2 * c, s + 2 * c);
+    for (int c = threadIdx.x; c < nch; c += 32 * WPC) cp_async16(dst + 2 * c, s + 2 * c);
   };
   stage(0);
   commit();
@@ -115,10 +121,14 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
   };
 
   for (int p = 0; p < ns; ++p) {
+    if (WPC > 1) __syncthreads();  // every warp is done with the slot stage(p + 1) overwrites
     if (p + 1 < ns) stage(p + 1);
     commit();
     wait_group<1>();
-    __syncwarp();
+    if (WPC > 1)
+      __syncthreads();
+    else
+      __syncwarp();
     const double* pr = ring + (p & 1) * SREC;
     const int mfirst = reinterpret_cast<const int*>(pr + 6 * NQ + 6)[1];
     while (mfirst >= base + FLUSH) {
@@ -218,22 +228,34 @@ __global__ void __launch_bounds__(32) k_assemble_row4(RegularArgs a) {
 }
 
 template <int WIN>
-static size_t row4_smem_bytes(int nq, int r) {
-  return (size_t)(row4::Shape<WIN>::WREG + row4::DEPTH * r * (6 * nq + 8)) * sizeof(double);
+static size_t row4_smem_bytes(int nq, int r, int wpc) {
+  return (size_t)(wpc * row4::Shape<WIN>::WREG + row4::DEPTH * r * (6 * nq + 8)) * sizeof(double);
 }
 
 template <int NQ, int WIN, int R, int FLUSH>
 static cudaError_t launch_row4_nq(const RegularArgs& a, int mode, cudaStream_t st) {
-  dim3 grid((a.n_rows + row4::ROWS - 1) / row4::ROWS, a.n_tiles);
-  const size_t smem = row4_smem_bytes<WIN>(NQ, R);
-  auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, 32, smem, st>>>(a);
-    return cudaGetLastError();
+  // warps per CTA sharing the record ring (HVB_ASM_WPC A/B; 4 by default)
+  static const int wpc_env = [] {
+    const char* e = getenv("HVB_ASM_WPC");
+    return e ? atoi(e) : 4;
+  }();
+  auto run = [&](auto wpc_tag) -> cudaError_t {
+    constexpr int WPC = decltype(wpc_tag)::value;
+    dim3 grid((a.n_rows + row4::ROWS * WPC - 1) / (row4::ROWS * WPC), a.n_tiles);
+    const size_t smem = row4_smem_bytes<WIN>(NQ, R, WPC);
+    auto go = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<grid, 32 * WPC, smem, st>>>(a);
+      return cudaGetLastError();
+    };
+    if (mode == 0) return go(k_assemble_row4<NQ, 0, WIN, R, FLUSH, WPC>);
+    if (mode == 1) return go(k_assemble_row4<NQ, 1, WIN, R, FLUSH, WPC>);
+    return go(k_assemble_row4<NQ, 2, WIN, R, FLUSH, WPC>);
   };
-  if (mode == 0) return go(k_assemble_row4<NQ, 0, WIN, R, FLUSH>);
-  if (mode == 1) return go(k_assemble_row4<NQ, 1, WIN, R, FLUSH>);
-  return go(k_assemble_row4<NQ, 2, WIN, R, FLUSH>);
+  if (wpc_env == 1) return run(std::integral_constant<int, 1>{});
+  if (wpc_env == 2) return run(std::integral_constant<int, 2>{});
+  if (wpc_env == 8) return run(std::integral_constant<int, 8>{});
+  return run(std::integral_constant<int, 4>{});
 }
 
 // window WIN, R records per lane per step, flush width 16 or 32: the
