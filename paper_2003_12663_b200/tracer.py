@@ -82,6 +82,19 @@ def surface_distance_device(dm, X_dev):
 ROUNDS_PER_SYNC = 16  # rounds enqueued between host reads of the counters
 
 
+def _morton_order(X: np.ndarray) -> np.ndarray:
+    """Permutation sorting points along a 3-d Morton (Z-order) curve."""
+    if len(X) < 2:
+        return np.arange(len(X))
+    lo, hi = X.min(axis=0), X.max(axis=0)
+    q = ((X - lo) / np.maximum(hi - lo, 1e-300) * 1023.0).astype(np.uint64)  # 10 bits per axis
+    code = np.zeros(len(X), dtype=np.uint64)
+    for b in range(10):
+        for d in range(3):
+            code |= ((q[:, d] >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + d)
+    return np.argsort(code, kind="stable")
+
+
 def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap: int = 64,
                  max_rounds: int | None = None) -> TraceResult:
     import torch
@@ -99,6 +112,14 @@ def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap:
     orient = np.asarray(orientations, dtype=np.float64).reshape(-1)
     if orient.shape != (L,):
         raise ValueError(f"{L} start points but {orient.size} orientations")
+    # trace in Morton order of the seeds: the request lists are compacted in
+    # roughly line order, so neighbouring lines share warps of the N-body and
+    # the far-group classification skip stays coherent.  Per-target results
+    # do not depend on the slot, so this changes no result; outputs are put
+    # back in the caller's order below.
+    order = _morton_order(starts)
+    starts = np.ascontiguousarray(starts[order])
+    orient = orient[order]
     f64 = dict(dtype=torch.float64, device=dev)
     i32 = dict(dtype=torch.int32, device=dev)
     n = max(1, L)
@@ -159,6 +180,12 @@ def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap:
     dinfo = torch.empty(n, **f64)
     _lib.call("hvb_trace_summary", _lib.ptr(state), L, _lib.ptr(info), _lib.ptr(dinfo), st)
     evals = int(counters[3].item())
+    if L > 1:  # back to the caller's line order
+        inv = torch.as_tensor(np.argsort(order), device=dev)
+        poly = poly[inv]
+        state = state.view(n, sbytes)[inv].reshape(-1)
+        info = info[inv]
+        dinfo = dinfo[inv]
     return TraceResult(polylines=poly, info=info[:L].cpu().numpy(), start_mag=dinfo[:L].cpu().numpy(), state=state,
                        cap=cap, rounds=rounds, field_points=evals)
 

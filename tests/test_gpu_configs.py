@@ -93,3 +93,27 @@ def test_cfg3_floating_conductor():
     res = np.linalg.norm(rhs - Ad @ np.concatenate([sol.u, sol.V])) / np.linalg.norm(rhs)
     assert res <= 1e-6
     assert 0.2 < sol.V[0] < 0.5  # the floating sphere settles between 1 V and ground
+
+
+def test_cfg4_full_size_sampled_rows_and_solve():
+    """Config 4 at the benchmark size (199,104 panels, N = 99,558, 79 GB):
+    evenly spaced rows, dielectric (ADL) rows and rows with deferred near
+    pairs against the oracle (the oracle cannot hold the matrix: SURVEY
+    8c), and the reference-semantics solve's true residual."""
+    from paper_2003_12663_b200 import assembly, fixtures
+    from paper_2003_12663_b200.solver import solve
+
+    m = fixtures.rod_plane_mesh(1.0)
+    assert m.n_triangles == 199104 and m.n_collocation == 99558
+    A, rhs = assembly.assemble(m)
+    near = assembly.LAST_NEAR_ROWS
+    n = m.n_collocation
+    diel = np.nonzero(m.row_kind_code == 2)[0]
+    rows = [np.linspace(0, n - 1, 48).astype(int), diel[:: max(1, len(diel) // 12)][:12]]
+    if near is not None and np.any(near > 0):
+        nr = np.nonzero(near > 0)[0]
+        rows.append(nr[:: max(1, len(nr) // 12)][:12])
+    rows = np.unique(np.concatenate(rows))
+    assert _rows_vs_oracle(m, A, rows) <= 1e-10
+    sol = solve(A, rhs)
+    assert sol.iterations > 0 and sol.residual <= 1e-8
