@@ -173,8 +173,9 @@ int hvb_field_singular(const double* nodes6, const int* tri_cols, const int* vc_
 
 /* K12-K14 -- device-resident field-line tracer (csrc/trace.cu).
  * state: n_lines opaque records of hvb_line_state_bytes() bytes.
- * geo: HOST pointer to 13 doubles = bbox centre (3), half extent x bbox_factor (3), diag,
- * h_min, h_max, l_max, rel_tol, surface_tol_frac, e_floor.
+ * geo: HOST pointer to 14 doubles = bbox centre (3), half extent x bbox_factor (3), diag,
+ * h_min, h_max, l_max, rel_tol, surface_tol_frac, e_floor, max_steps (0 =
+ * unbounded, as the reference; else lines end with termination 4 MaxSteps).
  * mode 0 initialises every line from starts/orient and requests E at the
  * start; mode 1 consumes E results (e_out/e_flag, indexed by the previous
  * request slots); mode 2 consumes surface distances (sd_out).  New E / SD

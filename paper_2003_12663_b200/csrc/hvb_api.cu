@@ -296,6 +296,7 @@ int hvb_trace_ctrl(void* state, int n_lines, const double* starts, const int* or
   a.rel_tol = geo[10];
   a.tol_frac = geo[11];
   a.e_floor = geo[12];
+  a.max_steps = (long long)geo[13];
   a.e_pts = e_pts;
   a.e_line = e_line;
   a.sd_pts = sd_pts;
@@ -334,6 +335,7 @@ int hvb_trace_round(void* state, int n_lines, const double* geo, double* cur_pts
   a.rel_tol = geo[10];
   a.tol_frac = geo[11];
   a.e_floor = geo[12];
+  a.max_steps = (long long)geo[13];
   a.e_pts = nxt_pts;
   a.e_line = nxt_line;
   a.sd_pts = sd_pts;

@@ -126,7 +126,7 @@ cudaError_t launch_field_singular(const double* nodes6, const int* tri_cols, con
 
 // ---- device tracer (trace.cu) ----
 constexpr int kPhaseStart = 0, kPhaseSD = 1, kPhaseStage = 2, kPhaseSnap = 4, kPhaseDone = 5;  // 3: unused
-constexpr int kSurfaceHit = 0, kWeakField = 1, kMaxLength = 2, kLeftDomain = 3;
+constexpr int kSurfaceHit = 0, kWeakField = 1, kMaxLength = 2, kLeftDomain = 3, kMaxSteps = 4;
 constexpr int kStatusRunning = 0, kStatusDone = 1, kStatusWeakStart = 2, kStatusCoincident = 3;
 
 struct LineState {        // 304 bytes, one per line, in HBM
@@ -134,7 +134,7 @@ struct LineState {        // 304 bytes, one per line, in HBM
   double k[7][3];         // stage tangents (k[0] = FSAL k1)
   double req[3];          // outstanding E request point
   double h, s, err, tol, d_surf, local_r, sign;
-  int phase, stage, npts, armed, term, status, slot, pad;
+  int phase, stage, npts, armed, term, status, slot, steps;  // steps: RK steps taken (max_steps)
 };
 
 struct TraceArgs {
@@ -145,6 +145,7 @@ struct TraceArgs {
   // geometry / parameters (reference trace_fieldline 258-268, TraceParams)
   double center[3], half[3];
   double diag, h_min, h_max, l_max, rel_tol, tol_frac, e_floor;
+  long long max_steps;    // 0: unbounded (reference); else end lines with kMaxSteps
   // request lists (compacted by atomics): E requests, SD requests
   double* e_pts;          // (n_lines, 3)
   int* e_line;

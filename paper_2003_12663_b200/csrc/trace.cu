@@ -140,6 +140,11 @@ HVB_DEV void loop_body(const TraceArgs& a, LineState& L, int line) {
       return;
     }
   }
+  if (a.max_steps > 0 && L.steps >= a.max_steps) {  // extension: bounded step budget
+    finish(a, L, kMaxSteps, kStatusDone);
+    return;
+  }
+  L.steps += 1;
   const double h_cap = L.d_surf > __dmul_rn(4.0, a.h_max) ? a.h_max : fmax(a.h_min, __dmul_rn(0.45, L.d_surf));
   L.h = fmin(fmin(L.h, h_cap), __dadd_rn(__dsub_rn(a.l_max, L.s), a.h_min));
   double xi[3];
@@ -167,6 +172,7 @@ __global__ void k_trace_ctrl(TraceArgs a, int mode) {
     L.status = kStatusRunning;
     L.s = 0.0;
     L.h = a.h_max;
+    L.steps = 0;
     request_e(a, L, line, L.x, kPhaseStart);
     a.state[line] = L;
     return;

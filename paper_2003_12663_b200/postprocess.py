@@ -44,6 +44,7 @@ SURFACE_HIT = "SurfaceHit"
 WEAK_FIELD = "WeakField"
 MAX_LENGTH = "MaxLength"
 LEFT_DOMAIN = "LeftDomain"
+MAX_STEPS = "MaxSteps"
 
 
 class TraceError(ValueError):
@@ -99,6 +100,11 @@ class TraceParams:
     e_floor: float = 0.0
     max_length_frac: float = 4.0
     bbox_factor: float = 1.5
+    # extension (not in the reference): end a line after this many Runge-Kutta
+    # steps (accepted + rejected) with termination "MaxSteps"; None = the
+    # reference's unbounded loop (a line hugging a surface it never armed
+    # against can crawl at h_min for millions of steps)
+    max_steps: int | None = None
 
 
 # ---------------------------------------------------------------------------

@@ -32,7 +32,7 @@ import numpy as np
 
 from . import _fp, _lib
 
-TERMINATIONS = ("SurfaceHit", "WeakField", "MaxLength", "LeftDomain")
+TERMINATIONS = ("SurfaceHit", "WeakField", "MaxLength", "LeftDomain", "MaxSteps")
 STATUS_RUNNING, STATUS_DONE, STATUS_WEAK_START, STATUS_COINCIDENT = 0, 1, 2, 3
 VERTEX_PROXIMITY = 1e-12
 _LOG = int(os.environ.get("HVB_TRACE_LOG", "0"))  # print progress every N rounds
@@ -60,9 +60,10 @@ def _geometry(mesh, params):
     center = 0.5 * (lo + hi)
     half = 0.5 * (hi - lo) * params.bbox_factor
     diag = float(_fp.norm3_fused(hi - lo))
+    max_steps = getattr(params, "max_steps", None)
     geo = np.concatenate([center, half, [diag, params.h_min_frac * diag, params.h_max_frac * diag,
                                          params.max_length_frac * diag, params.rel_tol, params.surface_tol_frac,
-                                         params.e_floor]])
+                                         params.e_floor, float(max_steps) if max_steps else 0.0]])
     return geo.astype(np.float64)
 
 
@@ -125,7 +126,7 @@ def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap:
     n = max(1, L)
     sbytes = _lib.lib().hvb_line_state_bytes()
     state = torch.zeros(n * sbytes, dtype=torch.uint8, device=dev)
-    geo = np.ascontiguousarray(_geometry(mesh, params))  # host parameters (13 doubles)
+    geo = np.ascontiguousarray(_geometry(mesh, params))  # host parameters (14 doubles)
     geo_p = geo.ctypes.data_as(ctypes.c_void_p)
     starts_d = torch.as_tensor(starts, **f64)
     orient_d = torch.as_tensor(np.where(orient >= 0, 1, -1).astype(np.int32), **i32)
@@ -194,7 +195,7 @@ def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap:
 LINE_STATE_DTYPE = np.dtype([("x", "<f8", 3), ("k", "<f8", (7, 3)), ("req", "<f8", 3), ("h", "<f8"), ("s", "<f8"),
                              ("err", "<f8"), ("tol", "<f8"), ("d_surf", "<f8"), ("local_r", "<f8"), ("sign", "<f8"),
                              ("phase", "<i4"), ("stage", "<i4"), ("npts", "<i4"), ("armed", "<i4"), ("term", "<i4"),
-                             ("status", "<i4"), ("slot", "<i4"), ("pad", "<i4")])
+                             ("status", "<i4"), ("slot", "<i4"), ("steps", "<i4")])
 
 
 def line_states(res: TraceResult) -> np.ndarray:

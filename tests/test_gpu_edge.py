@@ -109,3 +109,19 @@ def test_surface_field_subset_matches_full(sphere):
     idx = np.array([5, 0, 77, m.n_collocation - 1])
     np.testing.assert_array_equal(surface_field_magnitudes(m, sol, indices=idx), full[idx])
     assert surface_field_magnitudes(m, sol, indices=np.zeros(0, dtype=int)).shape == (0,)
+
+
+def test_max_steps_budget_extension(sphere):
+    from paper_2003_12663_b200.postprocess import TraceParams, trace_fieldlines
+
+    m, _, _, sol = sphere
+    # the inward line from 1.3 R takes many small steps towards the surface
+    free = trace_fieldlines(sol, m, np.array([[1.3, 0.1, 0.0]]), [-1])[0]
+    assert free.termination == "SurfaceHit" and len(free.points) > 4
+    capped = trace_fieldlines(sol, m, np.array([[1.3, 0.1, 0.0]]), [-1], params=TraceParams(max_steps=2))[0]
+    assert capped.termination == "MaxSteps" and len(capped.points) <= 3
+    np.testing.assert_array_equal(capped.points, free.points[: len(capped.points)])
+    # a budget the line never reaches changes nothing (reference semantics)
+    big = trace_fieldlines(sol, m, np.array([[1.3, 0.1, 0.0]]), [-1], params=TraceParams(max_steps=10 ** 6))[0]
+    np.testing.assert_array_equal(big.points, free.points)
+    assert big.termination == free.termination
