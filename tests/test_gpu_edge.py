@@ -125,3 +125,17 @@ def test_max_steps_budget_extension(sphere):
     big = trace_fieldlines(sol, m, np.array([[1.3, 0.1, 0.0]]), [-1], params=TraceParams(max_steps=10 ** 6))[0]
     np.testing.assert_array_equal(big.points, free.points)
     assert big.termination == free.termination
+
+
+def test_target_batching_is_invisible(sphere, monkeypatch):
+    """Batches larger than TARGET_BATCH run as several launches with the same
+    per-target results (including the near pairs of near-surface points)."""
+    from paper_2003_12663_b200 import postprocess
+
+    m, _, _, sol = sphere
+    rng = np.random.default_rng(9)
+    d = rng.standard_normal((300, 3))
+    P = np.vstack([rng.uniform(-2, 2, (300, 3)), 1.01 * d / np.linalg.norm(d, axis=1)[:, None]])
+    ref = postprocess.eval_efield_batch(sol, m, P)
+    monkeypatch.setattr(postprocess, "TARGET_BATCH", 128)
+    np.testing.assert_array_equal(postprocess.eval_efield_batch(sol, m, P), ref)
