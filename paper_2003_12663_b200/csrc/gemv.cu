@@ -141,6 +141,66 @@ __global__ void __launch_bounds__(GEMV_THREADS) k_gemv_f32(const float* __restri
   }
 }
 
+// Single-precision storage with 256-bit loads (8 floats per load): float32
+// partial sums over 8 columns (the reference reduces in float32,
+// src/assembly.py:388), accumulated in float64 across chunks; 2 rows per CTA.
+HVB_DEV void ld256f(const float* p, float* v) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(p));
+}
+
+template <int ROWS>
+__global__ void __launch_bounds__(GEMV_THREADS) k_gemv_f32_v8(const float* __restrict__ A, int64_t lda, int nrows,
+                                                              int ncols, const double* __restrict__ x,
+                                                              const double* __restrict__ left,
+                                                              double* __restrict__ y) {
+  const int r0 = blockIdx.x * ROWS;
+  const int tid = threadIdx.x;
+  double acc[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) acc[r] = 0.0;
+  const int n8 = ncols >> 3;
+  const float* rowp[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) rowp[r] = A + (int64_t)min(r0 + r, nrows - 1) * lda;
+  for (int k = tid; k < n8; k += GEMV_THREADS) {
+    float xf[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xf[j] = (float)x[8 * k + j];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      float a[8];
+      ld256f(rowp[r] + 8 * k, a);
+      float s = a[0] * xf[0];  // float partial over 8 columns (the reference reduces in float32)
+#pragma unroll
+      for (int j = 1; j < 8; ++j) s = fmaf(a[j], xf[j], s);
+      acc[r] += (double)s;
+    }
+  }
+  if (tid == 0) {
+    for (int c = 8 * n8; c < ncols; ++c) {
+      const float xv = (float)x[c];
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r) acc[r] += (double)(rowp[r][c] * xv);
+    }
+  }
+  __shared__ double red[ROWS][GEMV_THREADS / 32];
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    double v = warp_sum(acc[r]);
+    if (lane == 0) red[r][wid] = v;
+  }
+  __syncthreads();
+  if (tid < ROWS && r0 + tid < nrows) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < GEMV_THREADS / 32; ++w) s += red[tid][w];
+    y[r0 + tid] = left ? left[r0 + tid] * s : s;
+  }
+}
+
 // xp[k] = z[perm[k]] / right[perm[k]]   (right may be null)
 __global__ void k_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -197,7 +257,9 @@ static bool v4_ok(const void* A, int64_t lda, const double* x) {
 cudaError_t launch_gemv(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const double* x,
                         const double* left, double* y, cudaStream_t st) {
   if (nrows == 0) return cudaSuccess;
-  if (is_f32) {
+  if (is_f32 && lda % 8 == 0 && (reinterpret_cast<uintptr_t>(A) & 31) == 0) {
+    k_gemv_f32_v8<8><<<(nrows + 7) / 8, GEMV_THREADS, 0, st>>>((const float*)A, lda, nrows, ncols, x, left, y);
+  } else if (is_f32) {
     constexpr int R = 8;
     k_gemv_f32<R><<<(nrows + R - 1) / R, GEMV_THREADS, 0, st>>>((const float*)A, lda, nrows, ncols, x, left, y);
   } else if (v4_ok(A, lda, x)) {
