@@ -44,6 +44,7 @@ __all__ = [
     "matvec",
     "charge_row",
     "assemble_kernel_row",
+    "adl_chunk_sum",
     "save_matrix",
     "load_matrix",
     "KERNEL_SL",
@@ -448,25 +449,36 @@ def _neutrality_scales(mesh, k: int):
     return ep, 0.5 * ep
 
 
-def _weighted_adl_sum(mesh, dm, members, adl_scale, id_scale, chunk: int = 4096):
-    """sum_i w_i adl ADL_i + w_i id e_i over `members`, in DEVICE column
-    order: member ADL rows are assembled into a scratch block and reduced
-    over rows in a fixed order (chunk by chunk)."""
+NEUTRALITY_CHUNK = 4096  # members per partial sum of a neutrality / charge row
+
+
+def adl_chunk_sum(mesh, dm, mem, adl_scale, id_scale):
+    """Partial sum_i w_i adl ADL_i + w_i id e_i over one chunk of members, in
+    DEVICE column order (the unit the neutrality rows are split into)."""
     import torch
 
-    dev = dm.device
     n = mesh.n_collocation
     lda = -(-n // LDA_ALIGN) * LDA_ALIGN
-    acc = torch.zeros(n, dtype=torch.float64, device=dev)
-    counts = {"near": 0}
+    mem = np.asarray(mem, dtype=np.int64)
+    w = mesh.lumped_weights[mem]
+    scratch = torch.empty((len(mem), lda), dtype=torch.float64, device=dm.device)
+    plan = _plan(dm.device, mesh.colloc_points[mem], mesh.colloc_normals[mem], np.ones(len(mem), np.int64),
+                 mem, w * adl_scale, w * id_scale, np.arange(len(mem)) * lda)
+    _run_rows(dm, plan, scratch, {"near": 0})
+    return scratch[:, :n].sum(dim=0)
+
+
+def _weighted_adl_sum(mesh, dm, members, adl_scale, id_scale, chunk: int | None = None):
+    """sum_i w_i adl ADL_i + w_i id e_i over `members`, in DEVICE column
+    order: chunk partials (adl_chunk_sum) added in chunk order -- the same
+    order parallel.assemble_distributed uses when the chunks are spread over
+    ranks, so the row is bitwise independent of the GPU count."""
+    import torch
+
+    chunk = chunk or NEUTRALITY_CHUNK
+    acc = torch.zeros(mesh.n_collocation, dtype=torch.float64, device=dm.device)
     for c0 in range(0, len(members), chunk):
-        mem = np.asarray(members[c0:c0 + chunk], dtype=np.int64)
-        w = mesh.lumped_weights[mem]
-        scratch = torch.empty((len(mem), lda), dtype=torch.float64, device=dev)
-        plan = _plan(dev, mesh.colloc_points[mem], mesh.colloc_normals[mem], np.ones(len(mem), np.int64),
-                     mem, w * adl_scale, w * id_scale, np.arange(len(mem)) * lda)
-        _run_rows(dm, plan, scratch, counts)
-        acc += scratch[:, :n].sum(dim=0)
+        acc += adl_chunk_sum(mesh, dm, members[c0:c0 + chunk], adl_scale, id_scale)
     return acc
 
 
@@ -516,7 +528,7 @@ def assemble(mesh: SurfaceMesh, cfg: QuadConfig | None = None, n_blocks: int = 1
     return matrix, rhs
 
 
-def assemble_rows(mesh: SurfaceMesh, dm, start: int, stop: int, precision: str = "double"):
+def assemble_rows(mesh: SurfaceMesh, dm, start: int, stop: int, precision: str = "double", neutrality=None):
     """Device rows [start, stop) of the system (a row block of
     ``partition_rows``) as a (stop-start, lda) tensor in device column
     order, plus pair counts over its collocation rows.  Every row is computed
@@ -550,7 +562,10 @@ def assemble_rows(mesh: SurfaceMesh, dm, start: int, stop: int, precision: str =
             adl, ids = _neutrality_scales(mesh, k - n)
             row = A[k - start]
             row[n:size] = 0.0
-            row[:n] = _weighted_adl_sum(mesh, dm, mesh.floating_collocation(k - n), adl, ids)
+            if neutrality is not None:  # computed across ranks (parallel.assemble_distributed)
+                row[:n] = neutrality[k - n]
+            else:
+                row[:n] = _weighted_adl_sum(mesh, dm, mesh.floating_collocation(k - n), adl, ids)
         if precision == "single":
             A = A.to(torch.float32)
     return A, counts

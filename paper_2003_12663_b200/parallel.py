@@ -227,8 +227,45 @@ class DistributedMatrix:
         return _DistOperator(self)
 
 
+def _distributed_neutrality(mesh, dm, group, start: int, stop: int):
+    """Neutrality rows n+k of floating surfaces (reference _row_equation
+    src/assembly.py:441-468) with their member ADL rows spread over the
+    ranks: member chunk c of surface k goes to rank c mod world, the chunk
+    partials are all-gathered and the owner of row n+k adds them in chunk
+    order -- bitwise the single-process row (assembly._weighted_adl_sum)."""
+    import torch
+    import torch.distributed as dist
+
+    from .assembly import NEUTRALITY_CHUNK, _neutrality_scales, adl_chunk_sum
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = mesh.n_collocation
+    out = {}
+    for k in range(mesh.n_floating):
+        members = mesh.floating_collocation(k)
+        adl, ids = _neutrality_scales(mesh, k)
+        chunks = [members[c0:c0 + NEUTRALITY_CHUNK] for c0 in range(0, len(members), NEUTRALITY_CHUNK)]
+        per = -(-len(chunks) // world)
+        mine = torch.zeros((per, n), dtype=torch.float64, device=dm.device)
+        for j, c in enumerate(range(rank, len(chunks), world)):
+            mine[j] = adl_chunk_sum(mesh, dm, chunks[c], adl, ids)
+        host = dist.get_backend(group) == "gloo"
+        send = mine.cpu() if host else mine
+        buf = torch.empty((world * per, n), dtype=torch.float64, device=send.device)
+        dist.all_gather_into_tensor(buf, send, group=group)
+        if start <= n + k < stop:
+            buf = buf.to(dm.device)
+            acc = torch.zeros(n, dtype=torch.float64, device=dm.device)
+            for c in range(len(chunks)):  # chunk order: rank c % world, slot c // world
+                acc += buf[(c % world) * per + c // world]
+            out[k] = acc
+    return out
+
+
 def assemble_distributed(mesh, cfg=None, group=None, precision: str = "double", device=None):
-    """Assemble this rank's row block (rank r owns partition_rows(N, world)[r])."""
+    """Assemble this rank's row block (rank r owns partition_rows(N, world)[r]);
+    neutrality rows are computed across all ranks (_distributed_neutrality)."""
     import torch.distributed as dist
 
     from .assembly import _device_mesh
@@ -241,7 +278,8 @@ def assemble_distributed(mesh, cfg=None, group=None, precision: str = "double", 
     size = n + mesh.n_floating
     start, stop = split_range(size, world, rank)
     dm = _device_mesh(mesh, cfg, device)
-    A, counts = assemble_rows(mesh, dm, start, stop, precision)
+    neutrality = _distributed_neutrality(mesh, dm, group, start, stop) if mesh.n_floating else None
+    A, counts = assemble_rows(mesh, dm, start, stop, precision, neutrality=neutrality)
     store = DeviceStore(A, n, size, dm.perm, dm.tiling.perm, row0=start)
     mat = DistributedMatrix(n, mesh.n_floating, start, stop, group=group, store=store)
     mat.diagnostics = {"rows": (start, stop), "pairs_near_singular_local": counts["near"]}

@@ -145,3 +145,53 @@ def test_row_sharded_device_path_matches_single_process():
     for g, ln in zip(got, lines):
         assert g.shape == ln.points.shape
         np.testing.assert_allclose(g, ln.points, rtol=0, atol=1e-10)
+
+
+def _float_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from conftest import build_case
+        from paper_2003_12663_b200 import assembly
+        from paper_2003_12663_b200.parallel import assemble_distributed
+
+        assembly.NEUTRALITY_CHUNK = 16  # several chunks per surface, spread over both ranks
+        m = build_case("cfg3mini")
+        A, rhs = assemble_distributed(m)
+        n = m.n_collocation
+        row = A.store.host_rows(n - A.start, n - A.start + 1)[0] if A.start <= n < A.stop else None
+        out_q.put((rank, row))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+def test_distributed_neutrality_row_bitwise():
+    """The neutrality row's member ADL rows are split over the ranks and
+    recombined in chunk order: bitwise the single-process row."""
+    from conftest import build_case
+    from paper_2003_12663_b200 import assembly
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_float_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    rows = [r[1] for r in res if r[1] is not None]
+    assert len(rows) == 1
+    old = assembly.NEUTRALITY_CHUNK
+    assembly.NEUTRALITY_CHUNK = 16
+    try:
+        m = build_case("cfg3mini")
+        A, _ = assembly.assemble(m)
+        ref = A.row(m.n_collocation)
+    finally:
+        assembly.NEUTRALITY_CHUNK = old
+    np.testing.assert_array_equal(rows[0], ref)
