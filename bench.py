@@ -458,6 +458,29 @@ def run_b200(args):
     flops = regular_flops(mesh, near_rows, sl_rows, adl_rows)
     achieved = flops / reg_t / 1e12 if reg_t > 0 else 0.0
 
+    # near-surface field evaluation: every collocation point
+    # offset by 0.25 of its local circumradius along the normal -- ~6 deferred
+    # near-singular panels per point (composite rules of 512-3,072 nodes)
+    na, nb = split_range(n, world, rank)
+    _, loc_r = postprocess.surface_distance_batch(mesh, mesh.colloc_points[na:nb])
+    P_near = torch.as_tensor(mesh.colloc_points[na:nb] + (0.25 * loc_r)[:, None] * mesh.colloc_normals[na:nb],
+                             device=dev)
+    dmn = device_mesh(mesh)
+    u_dev, key = postprocess._u_device(sol, dmn)
+    src = postprocess._sources(dmn, u_dev, key)
+    postprocess.field_points_device(dmn, u_dev, src, P_near[:1024], False)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    En = postprocess.field_points_device(dmn, u_dev, src, P_near, False)
+    f1.record()
+    torch.cuda.synchronize(dev)
+    near_pairs_per_point = float(En.near_pairs) / max(1, len(P_near))
+    fvec = torch.tensor([f0.elapsed_time(f1) / 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(fvec, op=dist.ReduceOp.MAX)
+    t_near = float(fvec.item())
+    del En, P_near
+
     # GEMV roofline: stream this rank's row block a few times (untimed)
     A, rhs = assemble_distributed(mesh) if world > 1 else assemble(mesh)
     st = A.store
@@ -549,6 +572,9 @@ def run_b200(args):
             "gmres_solve_s": t_solve,
             "gmres_iterations": iters,
             "field_evals_per_s": args.points / t_field,
+            "field_near_surface": {"points": n, "evals_per_s": n / t_near,
+                                   "near_pairs_per_point_rank0": near_pairs_per_point,
+                                   "note": "every collocation point + 0.25 local R along its normal (SURVEY 8d)"},
             "phases_s": {"assembly": t_asm, "solve": t_solve, "field": t_field, "trace": t_trace,
                          "assembly_regular_kernel": reg_t},
             "trace": {"lines": min(args.lines, n), "lines_per_s": min(args.lines, n) / t_trace if t_trace else None,
