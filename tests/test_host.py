@@ -401,3 +401,33 @@ def test_public_api_mirrors_reference_init():
     missing = [n for n in names if not hasattr(pkg, n)]
     assert not missing, missing
     assert pkg.__version__ == "0.1.0"
+
+
+def test_import_alias_drop_in():
+    """INTEGRATION.md's alias: `hvbem` and its submodules resolve to the
+    drop-in, with the names the reference's tests import."""
+    import importlib
+    import sys
+
+    saved = {k: v for k, v in sys.modules.items() if k == "hvbem" or k.startswith("hvbem.")}
+    try:
+        sys.modules["hvbem"] = importlib.import_module("paper_2003_12663_b200")
+        for sub in ("mesh", "quadrature", "kernels", "assembly", "solver", "postprocess", "fixtures", "config"):
+            sys.modules[f"hvbem.{sub}"] = importlib.import_module(f"paper_2003_12663_b200.{sub}")
+        from hvbem.assembly import (KERNEL_ADL, KERNEL_SL, AssemblyError, RowBlock, SystemMatrix,  # noqa: F401
+                                    assemble, assemble_kernel_row, charge_row, load_matrix, matvec,
+                                    partition_rows, save_matrix)
+        from hvbem.fixtures import concentric_mesh, sphere_mesh  # noqa: F401
+        from hvbem.mesh import CurvedTriangle, _flat_circumcircle  # noqa: F401
+        from hvbem.postprocess import (FieldLine, IonizationModel, TraceError, TraceParams,  # noqa: F401
+                                       eval_efield, eval_potential, load_ionization_model, pick_start_points,
+                                       streamer_integral, surface_field_magnitudes, trace_fieldline,
+                                       write_fieldline_csv)
+        from hvbem.quadrature import (PairClass, QuadConfig, QuadratureError, classify_pair,  # noqa: F401
+                                      closest_point, closest_point_flat, duffy_rule, near_singular_rule,
+                                      regular_rule, subdivide_at)
+        from hvbem.solver import Solution, SolverConfig, SolverError, residual, solve  # noqa: F401
+    finally:
+        for k in [k for k in sys.modules if k == "hvbem" or k.startswith("hvbem.")]:
+            del sys.modules[k]
+        sys.modules.update(saved)
