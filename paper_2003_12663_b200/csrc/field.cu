@@ -31,7 +31,7 @@ __global__ void k_contract(const double* __restrict__ table, int nt, int nq, con
 
 
 
-constexpr int FT = 128;   // targets per CTA
+constexpr int FT = 256;   // targets per CTA
 constexpr int FCH = 32;   // panels per shared-memory chunk
 
 // One (target block bx, panel split by) tile of the N-body sum.  Called by
