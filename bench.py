@@ -529,9 +529,7 @@ def run_b200(args):
             reps.append([t1 - t0, t2 - t1, t3 - t2, t_dm - t0])
         ea, es, ef, eu = np.median(np.array(reps), axis=0).tolist()
         dmh = device_mesh(mesh)
-        h2d = int(sum(t.numel() * t.element_size() for t in (dmh.nodes6, dmh.tri_cols, dmh.ccr, dmh.points,
-                                                             dmh.normals, dmh.vc_ptr, dmh.vc_tri, dmh.vc_corner,
-                                                             dmh.cls)) + P_dev.numel() * 8 + N * 8)
+        h2d = dmh.h2d_bytes + P_dev.numel() * 8 + N * 8  # mesh + tiling arrays, field points, rhs
         d2h = int(n * 8 + E.size * 8)
         evec = torch.tensor([ea, es, ef, eu], dtype=torch.float64, device=dev)
         if world > 1:

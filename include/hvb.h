@@ -37,13 +37,26 @@ int hvb_build_table(const double* nodes6, int nt, int nq, const double* rule, do
 
 /* Pack the per-column-tile panel streams (one record per (tile, panel)
  * entry): sample table, circumcircle classification bracket thr = fl(eta*R),
- * owned local columns.  ent_meta = (mfirst, l0, l1, l2, flags) per entry.
+ * owned local columns.  ent_meta = (mfirst, l0, l1, l2, flags) per entry,
+ * l = local column of an owned corner or -1; the record stores l % window
+ * (window = the dump slot for -1).
  * centered = 0: 6*nq+8 doubles, nodes (y, w0..2); centered = 1: 8*nq+8,
  * nodes (-2(y-cc), |y-cc|^2, w0..2, 0) (not used by the shipped layouts).
  * Replaces: the
  * per-row classification setup of row_pass1  assembly.py:155-168 */
 int hvb_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
-                     const int* ent_meta, long long n_entries, int centered, double* stream_out, void* stream);
+                     const int* ent_meta, long long n_entries, int centered, int window, double* stream_out,
+                     void* stream);
+
+/* Per-panel device arrays from the flat circumcircles (cc (nt,3), R (nt)):
+ * ccr (nt,4) = cc, R; cls (nt,6) = cc, fl(eta R), fl(eta R)^2 (1 -+ 1e-13);
+ * groups (ceil(nt/32), 8) = bounds of aligned 32-panel groups (centre,
+ * rho_cls, rho_sd), equal bit for bit to device.py:panel_groups.
+ * Replaces: the per-triangle classification inputs of classify_pair
+ * quadrature.py:207-221 / assembly.py:155-168 and _surface_distance
+ * postprocess.py:198-218 (mesh circumcircles mesh.py:188-200) */
+int hvb_panel_data(const double* circumcenters, const double* radii, int nt, double eta, double* ccr, double* cls,
+                   double* groups, void* stream);
 
 /* K2+K3 -- regular sweep of n_rows collocation rows against every panel,
  * classification fused (regular iff ||x-cc|| > eta*R with the reference's

@@ -23,7 +23,8 @@ _D = ctypes.c_double
 # name -> argtypes (all return int status)
 SIGNATURES = {
     "hvb_build_table": [_P, _I, _I, _P, _P, _P],
-    "hvb_build_stream": [_P, _I, _P, _D, _P, _P, _LL, _I, _P, _P],
+    "hvb_build_stream": [_P, _I, _P, _D, _P, _P, _LL, _I, _I, _P, _P],
+    "hvb_panel_data": [_P, _P, _I, _D, _P, _P, _P, _P],
     "hvb_assemble_regular": [_P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _LL, _P],
     "hvb_assemble_singular": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "hvb_fill_float_cols": [_P, _P, _P, _I, _I, _I, _P],

@@ -39,11 +39,20 @@ int hvb_build_table(const double* nodes6, int nt, int nq, const double* rule, do
   return check(hvb::launch_build_table(nodes6, nt, nq, rule, table, (cudaStream_t)stream), "hvb_build_table");
 }
 
+int hvb_panel_data(const double* circumcenters, const double* radii, int nt, double eta, double* ccr, double* cls,
+                   double* groups, void* stream) {
+  if (nt < 0) return fail(HVB_EARG, "hvb_panel_data: negative panel count");
+  return check(hvb::launch_panel_data(circumcenters, radii, nt, eta, ccr, cls, groups, (cudaStream_t)stream),
+               "hvb_panel_data");
+}
+
 int hvb_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
-                     const int* ent_meta, long long n_entries, int centered, double* stream_out, void* stream) {
+                     const int* ent_meta, long long n_entries, int centered, int window, double* stream_out,
+                     void* stream) {
   if (n_entries < 0) return fail(HVB_EARG, "hvb_build_stream: negative entry count");
-  return check(hvb::launch_build_stream(table, nq, ccr, eta, ent_tri, ent_meta, n_entries, centered, stream_out,
-                                        (cudaStream_t)stream),
+  if (window < 1 || window > 32767) return fail(HVB_EARG, "hvb_build_stream: window out of range");
+  return check(hvb::launch_build_stream(table, nq, ccr, eta, ent_tri, ent_meta, n_entries, centered, window,
+                                        stream_out, (cudaStream_t)stream),
                "hvb_build_stream");
 }
 

@@ -89,7 +89,10 @@ cudaError_t launch_regular_row4(const RegularArgs& a, int nq, int mode, int wind
 cudaError_t launch_build_table(const double* nodes6, int nt, int nq, const double* rule, double* out,
                                cudaStream_t st);
 cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
-                                const int* ent_meta, int64_t ne, int centered, double* out, cudaStream_t st);
+                                const int* ent_meta, int64_t ne, int centered, int window, double* out,
+                                cudaStream_t st);
+cudaError_t launch_panel_data(const double* cc, const double* radii, int nt, double eta, double* ccr, double* cls,
+                              double* groups, cudaStream_t st);
 cudaError_t launch_singular(const SingularArgs& a, cudaStream_t st);
 cudaError_t launch_fill_float_cols(double* A, const int64_t* row_out, const int* row_float, int n_rows, int n,
                                    int n_fl, cudaStream_t st);

@@ -1,6 +1,7 @@
 // Assembly support kernels: regular-rule sample table (K1), panel-stream
 // packing, the singular Duffy pass (K4) and the floating columns (K6).  The
-// regular sweep itself is csrc/assemble_dual.cu.
+// regular sweep itself is csrc/assemble_row4.cu (csrc/assemble_quad.cu and
+// csrc/assemble_dual.cu are the measured alternatives).
 //
 // Reference: TriangleTables src/assembly.py:73-118, row_pass1 singular batch
 // 202-235, _row_equation 408-468.
@@ -28,6 +29,60 @@ __global__ void k_build_table(const double* __restrict__ nodes6, int nt, int nq,
   o[5] = jw * v;
 }
 
+// Per-panel device arrays from the circumcircles (one warp per aligned
+// group of 32 panels, the tail padded with the last panel):
+//   ccr    (nt, 4) = cc, R                          (surface distance, streams)
+//   cls    (nt, 6) = cc, thr = fl(eta R), thr^2 (1 -+ 1e-13)  (field kernels)
+//   groups (ng, 8) = C, rho_cls, rho_sd, 0, 0, 0    (device.py panel_groups)
+// with numpy's rounding order (no contraction), so the arrays equal the host
+// statement device.py:panel_groups bit for bit (tests/test_gpu_edge.py).
+__global__ void k_panel_data(const double* __restrict__ cc, const double* __restrict__ radii, int nt, double eta,
+                             double* __restrict__ ccr, double* __restrict__ cls, double* __restrict__ groups) {
+  const int lane = threadIdx.x & 31;
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (g >= (nt + 31) / 32) return;
+  const int i = g * 32 + lane;
+  const int t = min(i, nt - 1);
+  const double cx = cc[3 * (size_t)t], cy = cc[3 * (size_t)t + 1], cz = cc[3 * (size_t)t + 2];
+  const double R = radii[t];
+  const double thr = __dmul_rn(eta, R);
+  if (i < nt) {
+    double* o = ccr + 4 * (size_t)i;
+    o[0] = cx; o[1] = cy; o[2] = cz; o[3] = R;
+    const double t2 = __dmul_rn(thr, thr);
+    double* c = cls + 6 * (size_t)i;
+    c[0] = cx; c[1] = cy; c[2] = cz; c[3] = thr;
+    c[4] = __dmul_rn(t2, 1.0 - 1e-13);
+    c[5] = __dmul_rn(t2, 1.0 + 1e-13);
+  }
+  double lo[3] = {cx, cy, cz}, hi[3] = {cx, cy, cz};
+#pragma unroll
+  for (int o = 16; o; o >>= 1)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+  const double Cx = __dmul_rn(0.5, __dadd_rn(lo[0], hi[0]));
+  const double Cy = __dmul_rn(0.5, __dadd_rn(lo[1], hi[1]));
+  const double Cz = __dmul_rn(0.5, __dadd_rn(lo[2], hi[2]));
+  const double dx = __dsub_rn(cx, Cx), dy = __dsub_rn(cy, Cy), dz = __dsub_rn(cz, Cz);
+  const double d = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+  double rc = __dadd_rn(d, thr), rs = __dadd_rn(d, R);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    rc = fmax(rc, __shfl_xor_sync(0xffffffffu, rc, o));
+    rs = fmax(rs, __shfl_xor_sync(0xffffffffu, rs, o));
+  }
+  if (lane == 0) {
+    double* o = groups + 8 * (size_t)g;
+    o[0] = Cx; o[1] = Cy; o[2] = Cz;
+    o[3] = __dmul_rn(rc, 1.0 + 1e-12);
+    o[4] = __dmul_rn(rs, 1.0 + 1e-12);
+    o[5] = o[6] = o[7] = 0.0;
+  }
+}
+
 // Pack one stream record per (tile, panel) entry.
 // centered = 0: per node (y, w0, w1, w2) -- 6 doubles (dual / quad layouts).
 // centered = 1: per node (-2 (y - cc), |y - cc|^2, w0, w1, w2, 0) -- 8 doubles
@@ -41,7 +96,7 @@ __global__ void k_build_stream(const double* __restrict__ table, int nq,
                                const double* __restrict__ ccr,  // (nt,4): cc, R
                                double eta, const int* __restrict__ ent_tri,
                                const int* __restrict__ ent_meta,  // (ne,5): mfirst, slot0, slot1, slot2, flags
-                               int64_t ne, int centered, double* __restrict__ out) {
+                               int64_t ne, int centered, int window, double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= ne) return;
   const int per = centered ? 8 : 6;
@@ -81,7 +136,9 @@ __global__ void k_build_stream(const double* __restrict__ table, int nq,
   m[0] = t;
   m[1] = em[0];
   short* l = reinterpret_cast<short*>(m + 2);
-  for (int c = 0; c < 3; ++c) l[c] = (short)em[1 + c];  // window slots, computed on the host
+  // window slot of each owned corner (local column mod window); window =
+  // the dump slot for corners owned by another tile
+  for (int c = 0; c < 3; ++c) l[c] = (short)(em[1 + c] >= 0 ? em[1 + c] % window : window);
   l[3] = (short)em[4];
 }
 
@@ -159,12 +216,20 @@ cudaError_t launch_build_table(const double* nodes6, int nt, int nq, const doubl
   return cudaGetLastError();
 }
 
+cudaError_t launch_panel_data(const double* cc, const double* radii, int nt, double eta, double* ccr, double* cls,
+                              double* groups, cudaStream_t st) {
+  if (nt == 0) return cudaSuccess;
+  const int warps = (nt + 31) / 32;
+  k_panel_data<<<(warps + 3) / 4, 128, 0, st>>>(cc, radii, nt, eta, ccr, cls, groups);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, double eta,
-                                const int* ent_tri, const int* ent_meta, int64_t ne, int centered, double* out,
-                                cudaStream_t st) {
+                                const int* ent_tri, const int* ent_meta, int64_t ne, int centered, int window,
+                                double* out, cudaStream_t st) {
   if (ne == 0) return cudaSuccess;
   k_build_stream<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(table, nq, ccr, eta, ent_tri, ent_meta, ne, centered,
-                                                              out);
+                                                              window, out);
   return cudaGetLastError();
 }
 

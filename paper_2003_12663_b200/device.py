@@ -216,21 +216,31 @@ class DeviceMesh:
         i32 = dict(dtype=torch.int32, device=device)
         self.n = mesh.n_collocation
         self.nt = mesh.n_triangles
-        self.nodes6 = torch.as_tensor(mesh.tri_nodes.reshape(self.nt, 18), **f64).contiguous()
-        self.tri_cols = torch.as_tensor(mesh.tri_corner_cols, **i32).contiguous()
-        ccr = np.column_stack([mesh.circumcenters, mesh.circumradii])
-        self.ccr = torch.as_tensor(ccr, **f64).contiguous()
-        self.radii = torch.as_tensor(mesh.circumradii, **f64)
-        self.points = torch.as_tensor(mesh.colloc_points, **f64).contiguous()
-        self.normals = torch.as_tensor(mesh.colloc_normals, **f64).contiguous()
-        self.vc_ptr = torch.as_tensor(mesh.vc_ptr, **i32)
-        self.vc_tri = torch.as_tensor(mesh.vc_tri, **i32)
-        self.vc_corner = torch.as_tensor(mesh.vc_corner, **i32)
-        # classification bracket per panel (field kernels): cc, thr, lo, hi
-        thr = cfg.eta * mesh.circumradii
-        cls = np.column_stack([mesh.circumcenters, thr, thr * thr * (1 - 1e-13), thr * thr * (1 + 1e-13)])
-        self.cls = torch.as_tensor(cls, **f64).contiguous()
-        self.groups = torch.as_tensor(panel_groups(mesh.circumcenters, mesh.circumradii, thr), **f64).contiguous()
+        h2d = []  # host arrays copied to the device (bench.py e2e byte count)
+
+        def up(x, **kw):
+            t = torch.as_tensor(x, **kw).contiguous()
+            h2d.append(t.numel() * t.element_size())
+            return t
+
+        self.nodes6 = up(mesh.tri_nodes.reshape(self.nt, 18), **f64)
+        self.tri_cols = up(mesh.tri_corner_cols, **i32)
+        self.radii = up(mesh.circumradii, **f64)
+        self.points = up(mesh.colloc_points, **f64)
+        self.normals = up(mesh.colloc_normals, **f64)
+        self.vc_ptr = up(mesh.vc_ptr, **i32)
+        self.vc_tri = up(mesh.vc_tri, **i32)
+        self.vc_corner = up(mesh.vc_corner, **i32)
+        st = _lib.stream_ptr(device)
+        # per-panel classification arrays and the 32-panel group bounds, built
+        # on the device from the circumcircles (csrc/tables.cu k_panel_data;
+        # equal to the host statement panel_groups below)
+        cc = up(mesh.circumcenters, **f64)
+        self.ccr = torch.empty((self.nt, 4), **f64)     # cc, R
+        self.cls = torch.empty((self.nt, 6), **f64)     # cc, thr, lo, hi
+        self.groups = torch.empty((-(-self.nt // PANEL_GROUP), 8), **f64)
+        _lib.call("hvb_panel_data", _lib.ptr(cc), _lib.ptr(self.radii), self.nt, float(cfg.eta), _lib.ptr(self.ccr),
+                  _lib.ptr(self.cls), _lib.ptr(self.groups), st)
 
         # rule tables
         reg = regular_rule(cfg.regular_order)
@@ -243,7 +253,6 @@ class DeviceMesh:
         self.rule_graded = torch.as_tensor(
             _rule4(graded_rule(cfg.bisect_depth, cfg.near_duffy_points, cfg.near_outer_order)), **f64)
 
-        st = _lib.stream_ptr(device)
         # K1 sample table
         self.table = torch.empty((self.nt, self.nq, 6), **f64)
         _lib.call("hvb_build_table", _lib.ptr(self.nodes6), self.nt, self.nq, _lib.ptr(self.rule_regular),
@@ -254,23 +263,21 @@ class DeviceMesh:
         tiling = mesh_tiling(mesh, max_tile, WINDOW, STRIPS, GROUP, FLUSH)
         self.layout_bits = LAYOUT_BITS
         self.tiling = tiling
-        self.perm = torch.as_tensor(tiling.perm, **i32)
-        self.col_dev = torch.as_tensor(tiling.inv, **i32)
-        self.tile_ptr = torch.as_tensor(tiling.tile_ptr, dtype=torch.int64, device=device)
-        self.tile_col0 = torch.as_tensor(tiling.tile_col0, **i32)
-        self.tile_width = torch.as_tensor(tiling.tile_width, **i32)
-        ent_tri = torch.as_tensor(tiling.ent_tri, **i32)
-        meta = tiling.ent_meta.copy()
-        loc = meta[:, 1:4]
-        meta[:, 1:4] = np.where(loc >= 0, loc % WINDOW, WINDOW)  # window slots (WINDOW = dump slot)
-        ent_meta = torch.as_tensor(meta, **i32).contiguous()
+        self.perm = up(tiling.perm, **i32)
+        self.col_dev = up(tiling.inv, **i32)
+        self.tile_ptr = up(tiling.tile_ptr, dtype=torch.int64, device=device)
+        self.tile_col0 = up(tiling.tile_col0, **i32)
+        self.tile_width = up(tiling.tile_width, **i32)
+        ent_tri = up(tiling.ent_tri, **i32)
+        ent_meta = up(tiling.ent_meta, **i32)  # (mfirst, l0, l1, l2, flags); slots = l % WINDOW on the device
         ne = len(tiling.ent_tri)
         self.centered = CENTERED
         self.rec = (8 if CENTERED else 6) * self.nq + 8
         self.stream = torch.empty((ne, self.rec), **f64)
         _lib.call("hvb_build_stream", _lib.ptr(self.table), self.nq, _lib.ptr(self.ccr), float(cfg.eta),
-                  _lib.ptr(ent_tri), _lib.ptr(ent_meta), ne, int(CENTERED), _lib.ptr(self.stream), st)
+                  _lib.ptr(ent_tri), _lib.ptr(ent_meta), ne, int(CENTERED), WINDOW, _lib.ptr(self.stream), st)
         self.n_tiles = len(tiling.tile_width)
+        self.h2d_bytes = int(sum(h2d))
 
 
 PANEL_GROUP = 32  # csrc/field.cu FCH: panels per shared-memory batch / bound group

@@ -139,3 +139,38 @@ def test_target_batching_is_invisible(sphere, monkeypatch):
     ref = postprocess.eval_efield_batch(sol, m, P)
     monkeypatch.setattr(postprocess, "TARGET_BATCH", 128)
     np.testing.assert_array_equal(postprocess.eval_efield_batch(sol, m, P), ref)
+
+
+@pytest.mark.parametrize("maker", ["sphere", "rod_plane", "one_panel"])
+def test_device_panel_data_matches_host_statement(maker):
+    """k_panel_data (ccr, cls, 32-panel group bounds) equals the host
+    statement device.py:panel_groups and the numpy bracket bit for bit,
+    including a ragged last group; k_build_stream's window slots equal
+    l % WINDOW (dump slot WINDOW for corners owned by another tile)."""
+    import torch
+
+    from paper_2003_12663_b200 import device, fixtures
+    from paper_2003_12663_b200.mesh import parse_mesh
+    from paper_2003_12663_b200.quadrature import QuadConfig
+
+    if maker == "sphere":
+        m = fixtures.sphere_mesh(2)
+    elif maker == "rod_plane":
+        m = fixtures.rod_plane_mesh(0.1)
+    else:
+        m = parse_mesh("bemesh 1\nvertex 0 0 0 0\nvertex 1 1 0 0\nvertex 2 0 1 0\nvertex 3 0.5 0 0\n"
+                       "vertex 4 0.5 0.5 0\nvertex 5 0 0.5 0\ntriangle 0 1 2 3 4 5 0\npatch 0 electrode 1.0\n")
+    cfg = QuadConfig()
+    dm = device.DeviceMesh(m, cfg, torch.device("cuda:0"))
+    thr = cfg.eta * m.circumradii
+    cls = np.column_stack([m.circumcenters, thr, thr * thr * (1 - 1e-13), thr * thr * (1 + 1e-13)])
+    assert np.array_equal(dm.cls.cpu().numpy(), cls)
+    assert np.array_equal(dm.ccr.cpu().numpy(), np.column_stack([m.circumcenters, m.circumradii]))
+    assert np.array_equal(dm.groups.cpu().numpy(), device.panel_groups(m.circumcenters, m.circumradii, thr))
+    # record tails: slots
+    rec = dm.stream.cpu().numpy()
+    tail = np.ascontiguousarray(rec[:, dm.rec - 2:])
+    slots = tail.view(np.int16).reshape(len(rec), 8)[:, 4:7].astype(np.int64)
+    loc = dm.tiling.ent_meta[:, 1:4].astype(np.int64)
+    assert np.array_equal(slots, np.where(loc >= 0, loc % dm.window, dm.window))
+    assert dm.h2d_bytes > m.tri_nodes.nbytes
