@@ -127,7 +127,7 @@ def _check_points(mesh: SurfaceMesh, X: np.ndarray):
         tree = cKDTree(mesh.vertices)
         mesh._device_cache["kdtree"] = tree
     # bounded search: only candidates within 1e-9 matter (far queries are free)
-    dist, idx = tree.query(X, k=1, distance_upper_bound=1e-9)
+    dist, idx = tree.query(X, k=1, distance_upper_bound=1e-9, workers=-1)
     bad = np.nonzero(np.isfinite(dist))[0]
     for i in bad:
         d = _fp.norm3_axis(mesh.vertices - X[i][None, :])
@@ -255,13 +255,46 @@ def _eval_batch(solution, mesh, X, cfg, potential):
 
     cfg = cfg or QuadConfig()
     X = np.ascontiguousarray(np.asarray(X, dtype=np.float64).reshape(-1, 3))
-    _check_points(mesh, X)
-    dm = device_mesh(mesh, cfg)
-    u_dev, key = _u_device(solution, dm)
-    src = _sources(dm, u_dev, key)
-    X_dev = torch.as_tensor(X, device=dm.device)
-    out = field_points_device(dm, u_dev, src, X_dev, potential)
-    return out.cpu().numpy()
+    if len(X) <= 1024:
+        _check_points(mesh, X)
+        checker = None
+    else:
+        # the coincidence check (host kd-tree, GIL released) runs beside the
+        # device evaluation; a coincident point still raises, nothing is returned
+        checker = _CheckThread(mesh, X)
+    try:
+        dm = device_mesh(mesh, cfg)
+        u_dev, key = _u_device(solution, dm)
+        src = _sources(dm, u_dev, key)
+        X_dev = torch.as_tensor(X, device=dm.device)
+        out = field_points_device(dm, u_dev, src, X_dev, potential)
+        res = out.cpu().numpy()
+    finally:
+        if checker is not None:
+            checker.result()  # a coincident point raises first
+    return res
+
+
+class _CheckThread:
+    """_check_points on a worker thread; result() re-raises its error."""
+
+    def __init__(self, mesh, X):
+        import threading
+
+        self._err = None
+        self._t = threading.Thread(target=self._run, args=(mesh, X), daemon=True)
+        self._t.start()
+
+    def _run(self, mesh, X):
+        try:
+            _check_points(mesh, X)
+        except BaseException as e:  # noqa: BLE001 - re-raised in result()
+            self._err = e
+
+    def result(self):
+        self._t.join()
+        if self._err is not None:
+            raise self._err
 
 
 def eval_potential_batch(solution, mesh: SurfaceMesh, X, cfg: QuadConfig | None = None) -> np.ndarray:

@@ -184,6 +184,20 @@ def test_eval_at_vertex_rejected(sphere2_solved):
         eval_potential(sol, m, m.colloc_points[5])
 
 
+def test_batch_with_one_coincident_point_rejected(sphere2_solved):
+    """Large batches run the coincidence check beside the device evaluation;
+    one coincident point (a midside node) still raises and returns nothing."""
+    from paper_2003_12663_b200.postprocess import eval_efield_batch
+
+    m, _, _, sol = sphere2_solved
+    X = np.random.default_rng(3).uniform(-2, 2, (5000, 3))
+    X[4321] = m.vertices[-1]
+    with pytest.raises(ValueError, match="coincides"):
+        eval_efield_batch(sol, m, X)
+    X[4321] = [2.5, 0.0, 0.0]
+    assert np.all(np.isfinite(eval_efield_batch(sol, m, X)))
+
+
 def test_field_is_gradient_and_linear(sphere2_solved):
     from paper_2003_12663_b200.postprocess import eval_efield, eval_potential
     from paper_2003_12663_b200.solver import Solution
