@@ -140,7 +140,8 @@ int hvb_peer_wait(const unsigned long long* flags, int world, unsigned long long
 /* xp[k] = z[perm[k]] / right[perm[k]]  (perm/right may be NULL) */
 int hvb_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp, void* stream);
 
-/* K9 -- one Arnoldi orthogonalisation in one cooperative launch: modified
+/* K9 -- one Arnoldi orthogonalisation in one launch (a 16-CTA cluster with
+ * w in registers and DSMEM reductions for n <= 131072, else cooperative): modified
  * Gram-Schmidt of w (n) against rows V[0..j] (row pitch ldv) in order,
  * h[i] = V_i.w (accumulate = 1: h[i] += for the re-orthogonalisation pass),
  * norms = (||w|| before, ||w|| after); partial is scratch of

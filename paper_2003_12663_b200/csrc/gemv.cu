@@ -13,6 +13,8 @@
 // block partition (reference invariance, tests/test_assembly.py:72-78).
 #include <cooperative_groups.h>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "launch.cuh"
 
@@ -377,6 +379,136 @@ __global__ void __launch_bounds__(MGS_THREADS) k_mgs(const double* __restrict__ 
   }
 }
 
+// Cluster variant (the default when N <= 16 * 1024 * 8): ONE thread-block
+// cluster of 16 CTAs x 1024 threads (non-portable size, one CTA per SM).  Each
+// thread keeps its PER entries of w in registers for the whole launch and
+// reads each V_i entry once (the dot and the update share the load); the
+// per-projection reduction goes through distributed shared memory and the
+// hardware cluster barrier instead of a global-memory grid sync.  Every CTA
+// sums the 16 CTA partials in the same fixed order, so h_i is identical in
+// every CTA and the result is bitwise reproducible.
+constexpr int MGSC_CTAS = 16;
+
+template <int PER>
+__global__ void __launch_bounds__(MGS_THREADS) k_mgs_cluster(const double* __restrict__ V, long long ldv, int j,
+                                                             double* __restrict__ w, int n, double* __restrict__ h,
+                                                             double* __restrict__ norms, int accumulate) {
+  cgk::cluster_group cl = cgk::this_cluster();
+  __shared__ double s_red[MGS_THREADS / 32];
+  __shared__ double s_part[2];
+  __shared__ double s_val;
+  const int rank = (int)cl.block_rank();
+  const int chunk = (n + MGSC_CTAS - 1) / MGSC_CTAS;
+  const int a = min(n, rank * chunk), b = min(n, a + chunk);
+  const int lane = threadIdx.x & 31;
+  auto total = [&](double v, int slot) {
+    const double t = block_sum(v, s_red);
+    if (threadIdx.x == 0) s_part[slot] = t;
+    cl.sync();  // partials of every CTA visible (also a CTA barrier)
+    if (threadIdx.x < 32) {
+      double p = lane < MGSC_CTAS ? *cl.map_shared_rank(&s_part[slot], lane) : 0.0;
+      // fixed pairwise order over the 16 CTA partials
+#pragma unroll
+      for (int o = 1; o < MGSC_CTAS; o <<= 1) p += __shfl_down_sync(0xffffffffu, p, o);
+      if (threadIdx.x == 0) s_val = p;
+    }
+    __syncthreads();
+    return s_val;
+  };
+  double wr[PER];
+  double loc = 0.0;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int k = a + threadIdx.x + e * MGS_THREADS;
+    wr[e] = k < b ? w[k] : 0.0;
+    loc = fma(wr[e], wr[e], loc);
+  }
+  const double nb2 = total(loc, 0);
+  for (int i = 0; i <= j; ++i) {
+    const double* vi = V + (size_t)i * ldv;
+    double vr[PER];
+    loc = 0.0;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) {
+      const int k = a + threadIdx.x + e * MGS_THREADS;
+      vr[e] = k < b ? vi[k] : 0.0;
+      loc = fma(vr[e], wr[e], loc);
+    }
+    const double hi = total(loc, (i + 1) & 1);  // alternating slots: a slot is rewritten two barriers later
+#pragma unroll
+    for (int e = 0; e < PER; ++e) wr[e] = fma(-hi, vr[e], wr[e]);
+    if (rank == 0 && threadIdx.x == 0) h[i] = accumulate ? h[i] + hi : hi;
+  }
+  loc = 0.0;
+#pragma unroll
+  for (int e = 0; e < PER; ++e) {
+    const int k = a + threadIdx.x + e * MGS_THREADS;
+    if (k < b) w[k] = wr[e];
+    loc = fma(wr[e], wr[e], loc);
+  }
+  const double na2 = total(loc, (j + 2) & 1);
+  if (rank == 0 && threadIdx.x == 0) {
+    norms[0] = sqrt(nb2);
+    norms[1] = sqrt(na2);
+  }
+  cl.sync();  // no CTA leaves while a peer may still read its s_part
+}
+
+template <int PER>
+static cudaError_t launch_mgs_cluster(const double* V, long long ldv, int j, double* w, int n, double* h,
+                                      double* norms, int accumulate, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(k_mgs_cluster<PER>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(MGSC_CTAS);
+  cfg.blockDim = dim3(MGS_THREADS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = MGSC_CTAS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_mgs_cluster<PER>, V, ldv, j, w, n, h, norms, accumulate);
+}
+
+// 1: cluster path usable (HVB_MGS=coop forces the cooperative kernel)
+static int mgs_cluster_ok() {
+  static int ok = -1;
+  if (ok < 0) {
+    const char* env = getenv("HVB_MGS");
+    ok = 0;
+    if (!(env && strcmp(env, "coop") == 0)) {
+      int dev = 0, major = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+      if (major >= 9 &&
+          cudaFuncSetAttribute(k_mgs_cluster<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(MGSC_CTAS);
+        cfg.blockDim = dim3(MGS_THREADS);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = MGSC_CTAS;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, k_mgs_cluster<8>, &cfg) == cudaSuccess && clusters >= 1) ok = 1;
+      }
+      cudaGetLastError();  // clear a failed probe
+    }
+  }
+  return ok;
+}
+
 int mgs_grid() {
   static int g = 0;
   if (g == 0) {
@@ -394,6 +526,11 @@ int mgs_grid() {
 
 cudaError_t launch_mgs(const double* V, long long ldv, int j, double* w, int n, double* h, double* norms,
                        double* partial, int accumulate, cudaStream_t st) {
+  if (mgs_cluster_ok()) {
+    if (n <= MGSC_CTAS * MGS_THREADS * 2) return launch_mgs_cluster<2>(V, ldv, j, w, n, h, norms, accumulate, st);
+    if (n <= MGSC_CTAS * MGS_THREADS * 4) return launch_mgs_cluster<4>(V, ldv, j, w, n, h, norms, accumulate, st);
+    if (n <= MGSC_CTAS * MGS_THREADS * 8) return launch_mgs_cluster<8>(V, ldv, j, w, n, h, norms, accumulate, st);
+  }
   const int grid = mgs_grid();
   void* args[] = {(void*)&V, (void*)&ldv, (void*)&j, (void*)&w, (void*)&n, (void*)&h, (void*)&norms,
                   (void*)&partial, (void*)&accumulate};

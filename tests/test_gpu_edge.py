@@ -174,3 +174,48 @@ def test_device_panel_data_matches_host_statement(maker):
     loc = dm.tiling.ent_meta[:, 1:4].astype(np.int64)
     assert np.array_equal(slots, np.where(loc >= 0, loc % dm.window, dm.window))
     assert dm.h2d_bytes > m.tri_nodes.nbytes
+
+
+@pytest.mark.parametrize("n,j", [(1, 0), (1000, 5), (99558, 40), (16 * 1024 * 8, 3), (16 * 1024 * 8 + 7, 3)])
+def test_mgs_matches_host_gram_schmidt(n, j):
+    """hvb_mgs (cluster kernel up to 16*1024*8 entries, cooperative kernel
+    beyond) against modified Gram-Schmidt in float64 numpy, with the
+    re-orthogonalisation pass (accumulate) and a bitwise repeat."""
+    import torch
+
+    from paper_2003_12663_b200 import _lib
+
+    rng = np.random.default_rng(n + j)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, j + 1))) if n > j else (np.eye(n, j + 1), None)
+    V = torch.tensor(np.ascontiguousarray(Q.T), device="cuda:0")
+    w0 = rng.standard_normal(n)
+    partial = torch.empty(_lib.lib().hvb_mgs_partial_size(), dtype=torch.float64, device="cuda:0")
+
+    def run(accumulate, w, h):
+        norms = torch.empty(2, dtype=torch.float64, device="cuda:0")
+        _lib.call("hvb_mgs", _lib.ptr(V), n, j, _lib.ptr(w), n, _lib.ptr(h), _lib.ptr(norms), _lib.ptr(partial),
+                  accumulate, _lib.stream_ptr())
+        return norms.cpu().numpy()
+
+    w = torch.tensor(w0, device="cuda:0")
+    h = torch.zeros(j + 1, dtype=torch.float64, device="cuda:0")
+    nrm = run(0, w, h)
+    nrm2 = run(1, w, h)
+    # host statement
+    wh = w0.copy()
+    hh = np.zeros(j + 1)
+    for _ in range(2):
+        for i in range(j + 1):
+            c = Q[:, i] @ wh
+            hh[i] += c
+            wh -= c * Q[:, i]
+    scale = np.linalg.norm(w0)
+    assert np.allclose(h.cpu().numpy(), hh, rtol=0, atol=1e-12 * scale)
+    assert np.allclose(w.cpu().numpy(), wh, rtol=0, atol=1e-12 * scale)
+    assert abs(nrm[0] - scale) <= 1e-13 * scale and abs(nrm2[1] - np.linalg.norm(wh)) <= 1e-12 * scale
+    # bitwise repeat
+    w2 = torch.tensor(w0, device="cuda:0")
+    h2 = torch.zeros(j + 1, dtype=torch.float64, device="cuda:0")
+    run(0, w2, h2)
+    run(1, w2, h2)
+    assert torch.equal(w2, w) and torch.equal(h2, h)
