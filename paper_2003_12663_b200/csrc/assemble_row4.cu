@@ -28,10 +28,15 @@ __device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\
 template <int N>
 __device__ __forceinline__ void wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// one (row, record) classification: regular iff ||x - cc|| > fl(eta R)
-HVB_DEV bool regular(double sq, const double* cg) {
+// one (row, record) classification: regular iff ||x - cc|| > fl(eta R),
+// decided as the reference rounds it.  The bracket test uses the 3-op FMA
+// sum of squares: it is within 4 ulp of the unfused sum, far inside the
+// bracket's 1e-13 margins, so it decides exactly as the unfused sum would;
+// only a pair inside the bracket pays for the unfused sum and the IEEE sqrt.
+HVB_DEV bool regular(d3 d, const double* cg) {
+  const double sq = fma(d.z, d.z, fma(d.y, d.y, d.x * d.x));
   bool r = sq > cg[5];
-  if (!r && !(sq < cg[4])) r = __dsqrt_rn(sq) > cg[3];
+  if (!r && !(sq < cg[4])) r = __dsqrt_rn(sumsq_unfused(d)) > cg[3];
   return r;
 }
 }  // namespace row4
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(32 * WPC) k_assemble_row4(RegularArgs a) {
     for (int j = 0; j < R; ++j) {
       const double* cg = pr + j * REC + 6 * NQ;
       const bool valid = R * p + j < ne;
-      const bool reg = row4::regular(sumsq_unfused(sub_rn(X0, mk3(cg[0], cg[1], cg[2]))), cg);
+      const bool reg = row4::regular(sub_rn(X0, mk3(cg[0], cg[1], cg[2])), cg);
       if (!reg) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
       const int* meta = reinterpret_cast<const int*>(cg + 6);
       const unsigned sl = static_cast<unsigned>(meta[2]), sf = static_cast<unsigned>(meta[3]);
