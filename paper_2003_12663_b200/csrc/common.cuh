@@ -86,12 +86,16 @@ HVB_DEV double rsqrt2_newton(double r2) {
 // Classification "regular iff ||x - cc|| > eta R" exactly as the reference
 // decides it (sqrt of the unfused sum, strict compare against fl(eta*R)).
 // thr = fl(eta*R) and the squared bracket [lo, hi] are precomputed per
-// triangle; only pairs inside the bracket pay for the IEEE sqrt.
+// triangle.  The bracket test uses the 3-op FMA sum of squares (within 4 ulp
+// of the unfused sum, far inside the 1e-13 margins, so it decides as the
+// unfused sum would); only pairs inside the bracket pay for the unfused sum
+// and the IEEE sqrt.
 HVB_DEV bool is_regular(d3 x, d3 cc, double thr, double thr2_lo, double thr2_hi) {
-  double s = sumsq_unfused(sub_rn(x, cc));
+  const d3 d = sub_rn(x, cc);
+  const double s = fma(d.z, d.z, fma(d.y, d.y, d.x * d.x));
   if (s > thr2_hi) return true;
   if (s < thr2_lo) return false;
-  return __dsqrt_rn(s) > thr;
+  return __dsqrt_rn(sumsq_unfused(d)) > thr;
 }
 
 // Flat closest point (u*, v*) -- reference closest_point_flat,
