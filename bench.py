@@ -582,9 +582,9 @@ def run_b200(args):
                       "rank0_max_points": trace_stats.get("max_points"),
                       "note": "cfg5 on the step's own solution: surface |E|, top-k seeds, sign(E.n) orientation, "
                               "device RK45 tracer + streamer (air_demo.gas)"},
-            "roofline": {"bound": "fp64", "kernel": f"k_assemble_{device.LAYOUT}", "achieved": achieved,
+            "roofline": {"bound": "fp64", "kernel": "k_sweep", "achieved": achieved,
                          "peak": tflops_peak, "unit": "TFLOP/s", "frac": achieved / tflops_peak if tflops_peak else None,
-                         "traffic": _ncu_traffic(f"k_assemble_{device.LAYOUT}"), "peak_source": "measured DFMA kernel on this GPU (hvb_bench_dfma)"},
+                         "traffic": _ncu_traffic("k_sweep"), "peak_source": "measured DFMA kernel on this GPU (hvb_bench_dfma)"},
             "roofline_gemv": {"bound": "hbm", "kernel": "k_gemv_f64", "traffic": _ncu_traffic("k_gemv"), "achieved": gemv_bytes / t_gemv / 1e9,
                               "peak": read_gbs, "unit": "GB/s", "frac": gemv_bytes / t_gemv / 1e9 / read_gbs,
                               "frac_of_measured_copy": gemv_bytes / t_gemv / 1e9 / 6547.2,

@@ -36,17 +36,20 @@ int hvb_version(void);
 int hvb_build_table(const double* nodes6, int nt, int nq, const double* rule, double* table, void* stream);
 
 /* Pack the per-column-tile panel streams (one record per (tile, panel)
- * entry): sample table, circumcircle classification bracket thr = fl(eta*R),
- * owned local columns.  ent_meta = (mfirst, l0, l1, l2, flags) per entry,
- * l = local column of an owned corner or -1; the record stores l % window
- * (window = the dump slot for -1).
- * centered = 0: 6*nq+8 doubles, nodes (y, w0..2); centered = 1: 8*nq+8,
- * nodes (-2(y-cc), |y-cc|^2, w0..2, 0) (not used by the shipped layouts).
- * Replaces: the
- * per-row classification setup of row_pass1  assembly.py:155-168 */
+ * entry; hvb_stream_record_doubles(nq, mode) doubles each): nodes, then an
+ * 8-double tail = cc, thr = fl(eta*R), squared classification bracket,
+ * panel id, first owned column, window slots of the owned corners, flags.
+ * ent_meta = (mfirst, l0, l1, l2, flags) per entry, l = local column of an
+ * owned corner or -1; the record stores l % window (window = the dump slot
+ * for -1).  mode 0 (SL stream): per node pair 10 doubles, per node
+ * Y = -2 s (y - cc), P = s |y - cc|^2, Q = s with s = (4 pi / jw)^2;
+ * mode 1 (ADL stream): per node (y, jw hat_0..2 / 4 pi).
+ * Replaces: the per-row classification setup and the sample tables of
+ * row_pass1  assembly.py:155-200 */
 int hvb_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
-                     const int* ent_meta, long long n_entries, int centered, int window, double* stream_out,
+                     const int* ent_meta, long long n_entries, int mode, int window, double* stream_out,
                      void* stream);
+int hvb_stream_record_doubles(int nq, int mode);
 
 /* Per-panel device arrays from the flat circumcircles (cc (nt,3), R (nt)):
  * ccr (nt,4) = cc, R; cls (nt,6) = cc, fl(eta R), fl(eta R)^2 (1 -+ 1e-13);
@@ -60,23 +63,17 @@ int hvb_panel_data(const double* circumcenters, const double* radii, int nt, dou
 
 /* K2+K3 -- regular sweep of n_rows collocation rows against every panel,
  * classification fused (regular iff ||x-cc|| > eta*R with the reference's
- * rounding), SL (kind 0) or ADL (kind 1) kernel, each entry written once
- * as row_scale * sum, for row-list entries [row_begin, row_begin+n_rows).
- * Non-regular, non-singular pairs are appended to
- * near_list as (row-list index, triangle).  mode: 0 all-SL, 1 all-ADL,
- * 2 mixed; | W << 8 = W-column window (row4: 40, 48, 56, 64), else | 4 =
- * 64-column window, else 96; | R << 16 = R records per lane (row layouts:
- * 4 or 8; the stream band is bounded over groups of R); | 1 << 20 = row
- * layouts flush 16 columns at a time (band <= window - 16, else - 32). | 8 = quad layout (the panel
- * stream's band is bounded over groups of 4 records, else 2); | 16 = row4
- * layout (lane = row, 4 records per lane; same stream as quad); | 32 = row8
- * (8 records per lane, band over groups of 8).
+ * rounding), SL (mode 0, SL stream) or ADL (mode 1, ADL stream) kernel,
+ * each entry written once as row_scale * sum, for row-list entries
+ * [row_begin, row_begin+n_rows).  hats (HOST pointer) = nq x 3 hat values
+ * hat_c(q) of the regular rule.  Non-regular, non-singular pairs are
+ * appended to near_list as (row-list index, triangle).
  * Replaces: row_pass1 regular part  assembly.py:170-200 and
  * _kernel_values 126-132 */
 int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_col0,
-                         const int* tile_width, int n_tiles, int nq, int row_begin, int n_rows, const double* rowdata,
-                         const int* row_kind, const int* row_col, const double* row_scale,
-                         const long long* row_out, double* A, const int* tri_cols, int mode, int warps_per_block,
+                         const int* tile_width, int n_tiles, int nq, const double* hats, int row_begin, int n_rows,
+                         const double* rowdata, const int* row_col, const double* row_scale,
+                         const long long* row_out, double* A, const int* tri_cols, int mode,
                          int* near_list, unsigned long long* near_count, long long near_cap, void* stream);
 
 /* K4 (+K6 diagonal) -- singular corner pairs with the split-corner Duffy
@@ -107,9 +104,12 @@ int hvb_near_apply_rows(const int* seg_ptr, int n_seg, const int* pairs, const d
                         const int* tri_cols, const int* col_dev, const double* row_scale, const long long* row_out,
                         double* A, void* stream);
 
-/* K8 -- y = left .* (A xp), A row-major (lda % 4 == 0), f64 or f32 storage.
+/* K8 -- y = left .* (A xp), A row-major (lda % 4 == 0).  prec 0: double
+ * storage; 1: float storage with float32 products and sums (the
+ * reference's float32 dot, assembly.py:386-392); 2: float storage, float32
+ * partials over 8 columns accumulated in double (opt-in).
  * Replaces: matvec  assembly.py:376-400 (inside solver op, solver.py:116-118) */
-int hvb_gemv(const void* A, int is_f32, long long lda, int n_rows, int n_cols, const double* x, const double* left,
+int hvb_gemv(const void* A, int prec, long long lda, int n_rows, int n_cols, const double* x, const double* left,
              double* y, void* stream);
 
 /* Fused GEMV + all-gather (row-sharded GMRES): as hvb_gemv
@@ -249,12 +249,7 @@ int hvb_streamer(const double* out_pts, const void* state, int n_lines, int cap,
 /* Roofline denominators measured on the box (bench.py): DFMA throughput
  * kernel (blocks x 256 threads x iters x 64 FMAs) and a read-only stream. */
 int hvb_bench_dfma(double* out, int blocks, int iters, void* stream);
-int hvb_bench_latency(double* out, int n, void* stream);
-int hvb_bench_nodes(double* out, int var, int blocks, int threads, int iters, void* stream);
 int hvb_bench_read(const double* p, long long n, double* out, int blocks, void* stream);
-int hvb_bench_rsqrt(const double* r2, int n, double* out, void* stream);
-int hvb_bench_gemv(const double* A, long long lda, int nrows, int ncols, const double* x, double* y, int variant,
-                   void* stream);
 
 #ifdef __cplusplus
 }

@@ -546,11 +546,11 @@ _DPB4 = np.array([5179 / 57600, 0.0, 7571 / 16695, 393 / 640, -92097 / 339200, 1
 
 
 def trace_line(mesh, u, start, orientation=1, rel_tol=1e-6, h_min_frac=1e-6, h_max_frac=0.05, surface_tol_frac=0.1,
-               e_floor=0.0, max_length_frac=4.0, bbox_factor=1.5, cfg=None, efield=None):
+               e_floor=0.0, max_length_frac=4.0, bbox_factor=1.5, cfg=None, efield=None, tables=None):
     """Dormand-Prince 5(4) on the unit tangent (postprocess.py:244-357).
     Returns (points (m,3), |E| (m,), arcs (m,), termination).  ``efield``
     overrides the field evaluator (default: oracle kernel rows)."""
-    tab = Tables(mesh, {**DEFAULT_CFG, **(cfg or {})}["regular_order"])
+    tab = tables or Tables(mesh, {**DEFAULT_CFG, **(cfg or {})}["regular_order"])
     ev = efield or (lambda p: efield_points(mesh, u, p[None], cfg, tab)[0])
     lo, hi = mesh.vertices.min(axis=0), mesh.vertices.max(axis=0)
     center, half = 0.5 * (lo + hi), 0.5 * (hi - lo) * bbox_factor

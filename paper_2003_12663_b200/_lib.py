@@ -25,7 +25,7 @@ SIGNATURES = {
     "hvb_build_table": [_P, _I, _I, _P, _P, _P],
     "hvb_build_stream": [_P, _I, _P, _D, _P, _P, _LL, _I, _I, _P, _P],
     "hvb_panel_data": [_P, _P, _I, _D, _P, _P, _P, _P],
-    "hvb_assemble_regular": [_P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _LL, _P],
+    "hvb_assemble_regular": [_P, _P, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _P, _LL, _P],
     "hvb_assemble_singular": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "hvb_fill_float_cols": [_P, _P, _P, _I, _I, _I, _P],
     "hvb_near_pairs": [_P, _LL, _P, _P, _P, _P, _P, _I, _P, _I, _I, _D, _P, _P],
@@ -55,11 +55,7 @@ SIGNATURES = {
     "hvb_near_coincide": [_P, _LL, _P, _P, _D, _P, _P],
     "hvb_streamer": [_P, _P, _I, _I, _P, _P, _I, _D, _P, _P, _P],
     "hvb_bench_dfma": [_P, _I, _I, _P],
-    "hvb_bench_latency": [_P, _I, _P],
-    "hvb_bench_nodes": [_P, _I, _I, _I, _I, _P],
     "hvb_bench_read": [_P, _LL, _P, _I, _P],
-    "hvb_bench_rsqrt": [_P, _I, _P, _P],
-    "hvb_bench_gemv": [_P, _LL, _I, _I, _P, _P, _I, _P],
 }
 
 HVB_EARG = 1
@@ -102,6 +98,8 @@ def lib():
             h.hvb_mgs_partial_size.argtypes = []
             h.hvb_ipc_handle_bytes.restype = _I
             h.hvb_ipc_handle_bytes.argtypes = []
+            h.hvb_stream_record_doubles.restype = _I
+            h.hvb_stream_record_doubles.argtypes = [_I, _I]
             _lib = h
     return _lib
 

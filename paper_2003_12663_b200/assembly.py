@@ -22,7 +22,7 @@ floating columns.
 
 from __future__ import annotations
 
-import os
+import ctypes
 import struct
 from dataclasses import dataclass, field
 
@@ -57,6 +57,10 @@ KERNEL_SL = "sl"
 KERNEL_ADL = "adl"
 KERNEL_E = "efield"
 LDA_ALIGN = 32  # row pitch in elements (256-byte aligned rows for the GEMV)
+# precision="single" matrices: False (default) reduces every row in float32
+# as the reference's float32 dot does; True keeps float32 products but sums
+# in double (more accurate, not the reference's arithmetic)
+SINGLE_SUMS_F64 = False
 
 
 class AssemblyError(RuntimeError):
@@ -127,6 +131,15 @@ class DeviceStore:
         import torch
 
         return self.A.dtype == torch.float32
+
+    @property
+    def prec(self) -> int:
+        """hvb_gemv storage/summation code: 0 double; 1 float32 storage with
+        the reference's float32 row sums (src/assembly.py:386-392); 2 float32
+        storage with double sums (opt-in, SINGLE_SUMS_F64)."""
+        if not self.is_f32:
+            return 0
+        return 2 if SINGLE_SUMS_F64 else 1
 
     def host_rows(self, start: int, stop: int) -> np.ndarray:
         dev = self.A[start:stop, : self.size].cpu().numpy()
@@ -268,7 +281,7 @@ def device_matvec(st: DeviceStore, z, right=None, left=None, out=None):
     s = _lib.stream_ptr(dev)
     rows = st.A.shape[0]
     y = out if out is not None else torch.empty(rows, dtype=torch.float64, device=dev)
-    _lib.call("hvb_gemv", _lib.ptr(st.A), int(st.is_f32), st.lda, rows, st.size, _lib.ptr(xp),
+    _lib.call("hvb_gemv", _lib.ptr(st.A), st.prec, st.lda, rows, st.size, _lib.ptr(xp),
               _lib.ptr(left), _lib.ptr(y), s)
     return y
 
@@ -346,19 +359,23 @@ def _span(label, e0):
         PROFILE.append((label, e0, _mark()))
 
 
-# warps per CTA of the regular sweep (csrc/assemble_dual.cu; ~29 KB of
-# shared memory per warp -> 7 resident warps per SM with 1-warp CTAs)
-_WPB = int(os.environ.get("HVB_ASM_WPB", "1"))
-
-
-def _run_rows(dm, plan: RowPlan, A, counts: dict, warps_per_block: int = 4):
+def _run_rows(dm, plan: RowPlan, A, counts: dict):
     """Regular + near + singular passes for one row plan writing into A."""
     import torch
 
     dev = dm.device
-    s = _lib.stream_ptr(dev)
     if plan.m == 0:
         return
+    with torch.cuda.device(dev):
+        _run_rows_on(dm, plan, A, counts)
+
+
+def _run_rows_on(dm, plan: RowPlan, A, counts: dict):
+    import torch
+
+    dev = dm.device
+    s = _lib.stream_ptr(dev)
+    hats = dm.hats.ctypes.data_as(ctypes.c_void_p)
     cap = max(4096, 16 * plan.m)
     e_reg = _mark()
     while True:
@@ -367,13 +384,10 @@ def _run_rows(dm, plan: RowPlan, A, counts: dict, warps_per_block: int = 4):
         for lo, hi, mode in ((0, plan.n_sl, 0), (plan.n_sl, plan.m, 1)):
             if hi > lo:
                 _lib.call(
-                    "hvb_assemble_regular", _lib.ptr(dm.stream), _lib.ptr(dm.tile_ptr), _lib.ptr(dm.tile_col0),
-                    _lib.ptr(dm.tile_width), dm.n_tiles, dm.nq, lo, hi - lo, _lib.ptr(plan.rowdata),
-                    _lib.ptr(plan.kind), _lib.ptr(plan.col), _lib.ptr(plan.scale), _lib.ptr(plan.out),
-                    _lib.ptr(A), _lib.ptr(dm.tri_cols), mode | (dm.window << 8 if dm.layout_bits & 48 else (4 if dm.window == 64 else 0)) | dm.layout_bits,
-                    _WPB,
-                    _lib.ptr(near), _lib.ptr(cnt),
-                    cap, s)
+                    "hvb_assemble_regular", _lib.ptr(dm.stream_for(mode)), _lib.ptr(dm.tile_ptr),
+                    _lib.ptr(dm.tile_col0), _lib.ptr(dm.tile_width), dm.n_tiles, dm.nq, hats, lo, hi - lo,
+                    _lib.ptr(plan.rowdata), _lib.ptr(plan.col), _lib.ptr(plan.scale), _lib.ptr(plan.out),
+                    _lib.ptr(A), _lib.ptr(dm.tri_cols), mode, _lib.ptr(near), _lib.ptr(cnt), cap, s)
         n_near = int(cnt.item())
         if n_near <= cap:
             break

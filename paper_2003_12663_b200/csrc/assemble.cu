@@ -1,0 +1,343 @@
+// Regular sweep (K2+K3 of SURVEY 2.2): reference row_pass1's regular pass
+// (src/assembly.py:155-200) for a tile of rows x one column tile.
+//
+// Work split.  A CTA owns WPC x 32 rows (lane = row) and one column tile;
+// its warps share one ring of panel records, staged by the bulk-copy engine
+// (cp.async.bulk, one copy of R = 4 consecutive records per stage, completion
+// on an mbarrier).  A stage is refilled by the LAST warp that releases it (a
+// shared-memory counter), so warps are not lock-stepped by CTA barriers and
+// drift up to S stages apart.  Every lane evaluates all R records of a stage
+// for its row (R independent FP64 chains), adds the three corner sums into
+// its row of a 48-column shared-memory window (record order: no atomics,
+// bitwise reproducible) and finished groups of 16 columns are flushed once.
+//
+// Record formats (csrc/tables.cu k_build_stream):
+//  * SL (MODE 0): per node pair 10 doubles [Yx0 Yy0 | Yz0 P0 | Q0 Q1 | Yx1 Yy1
+//    | Yz1 P1] with, per node q of panel t (cc = circumcentre, w = jw/4pi):
+//      s = 1/w^2,  Y = -2 s (y - cc),  P = s |y - cc|^2,  Q = s.
+//    With x' = x - cc (computed anyway for the classification) and X = |x'|^2
+//      r2' = x'.Y + X Q + P = s |x - y|^2 = (|x - y| / w)^2     (4 DFMA)
+//    and rsqrt2(r2') = 2 w / |x - y| (MUFU seed + 3 ops), so a node costs 10
+//    FP64 ops instead of 12: the hat functions hat_c(q) are kernel-parameter
+//    constants.  Regular pairs have |x'| > 1.2 R >= |y - cc| + 0.2 R, so the
+//    expansion loses at most ~120 ulp of r2 (~3e-14 relative).
+//  * ADL (MODE 1): per node 6 doubles (y, w hat_0, w hat_1, w hat_2).
+// Both end in an 8-double tail: cc, fl(eta R), bracket lo/hi, panel id,
+// first owned column, window slots of the 3 corners, flags.
+#include <cstdint>
+
+#include "launch.cuh"
+
+namespace hvb {
+namespace sweep {
+constexpr int ROWS = 32;
+constexpr int STRIDE = 33;
+constexpr int WIN = 48;                                  // window columns
+constexpr int SLOTS = WIN + 1;                           // + dump slot
+constexpr int WREG = (SLOTS * STRIDE + 1) & ~1;          // doubles per warp window (16-byte aligned)
+constexpr int FLUSH = 16;                                // columns per flush (band <= WIN - FLUSH)
+constexpr int R = 4;                                     // records per stage
+constexpr int WPC = 8;                                   // warps per CTA
+constexpr int S = 3;                                     // ring stages
+
+template <int NQ, int MODE>
+struct Rec {
+  static constexpr int NQP = MODE == 0 ? (NQ + 1) & ~1 : NQ;  // SL: node pairs (odd NQ padded)
+  static constexpr int DOUBLES = (MODE == 0 ? 5 : 6) * NQP + 8;
+  static constexpr int TAIL = DOUBLES - 8;
+};
+
+HVB_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+HVB_DEV void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+HVB_DEV void mbar_wait(uint64_t* bar, unsigned phase) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(phase)
+        : "memory");
+  }
+}
+
+// bulk copy global -> shared (the TMA engine's 1-D mode), completing on bar
+HVB_DEV void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// one (row, record) classification: regular iff ||x - cc|| > fl(eta R),
+// decided as the reference rounds it.  sq is the 3-op FMA sum of squares
+// (within 4 ulp of the unfused sum, far inside the bracket's 1e-13 margins,
+// so the bracket decides as the unfused sum would); only a pair inside the
+// bracket pays for the unfused sum and the IEEE sqrt.
+HVB_DEV bool regular(d3 d, double sq, const double* tail) {
+  bool r = sq > tail[5];
+  if (!r && !(sq < tail[4])) r = __dsqrt_rn(sumsq_unfused(d)) > tail[3];
+  return r;
+}
+}  // namespace sweep
+
+template <int NQ, int MODE>
+__global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
+  using namespace sweep;
+  using RC = Rec<NQ, MODE>;
+  constexpr int REC = RC::DOUBLES;
+  extern __shared__ __align__(16) double smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);         // S mbarriers
+  unsigned* released = reinterpret_cast<unsigned*>(smem + S);  // S release counters
+  double* ring = smem + 2 * S;                                 // S x R x REC
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  double* win = ring + S * R * REC + wib * WREG;
+
+  const int cta_row0 = blockIdx.x * (WPC * ROWS);
+  const int live_warps = min(WPC, (a.n_rows - cta_row0 + ROWS - 1) / ROWS);
+  const int tile = blockIdx.y;
+  const int64_t e0 = a.tile_ptr[tile], e1 = a.tile_ptr[tile + 1];
+  const int col0 = a.tile_col0[tile], width = a.tile_width[tile];
+  const double* src = a.stream + e0 * REC;
+  const int ne = (int)(e1 - e0);
+  const int ns = (ne + R - 1) / R;
+
+  auto issue = [&](int p) {  // one thread: stage p of this tile into ring slot p % S
+    const int nrec = min(R, ne - R * p);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    bulk_load(ring + (p % S) * (R * REC), src + (size_t)(R * p) * REC, (unsigned)(nrec * REC * 8), full + p % S);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      released[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int p = 0; p < min(S, ns); ++p) issue(p);
+  if (wib >= live_warps) return;  // no live rows: this warp takes no part in the ring
+
+  const int base_row = cta_row0 + wib * ROWS;
+  const int i0 = base_row + lane;
+  const bool live0 = i0 < a.n_rows;
+  const int lr0 = a.row_begin + (live0 ? i0 : a.n_rows - 1);
+  const double* rd0 = a.rowdata + 6 * (size_t)lr0;
+  const d3 X0 = mk3(rd0[0], rd0[1], rd0[2]);
+  const d3 N0 = mk3(rd0[3], rd0[4], rd0[5]);
+  const int own0 = a.row_col[lr0];
+  const int64_t fout = live0 ? a.row_out[lr0] : -1;
+  const double fscale = a.row_scale[lr0] * (MODE == 0 ? 0.5 : 1.0);  // SL sums hold 2w/r (exact halving)
+
+  for (int k = lane; k < SLOTS * STRIDE; k += 32) win[k] = 0.0;
+
+  int base = 0;
+  // flush 16 finished columns: lanes 0-15 write rows 0-15 and lanes 16-31
+  // rows 16-31 of 16 consecutive columns (128-byte row segments), so the
+  // window only needs band + 16 columns (48 columns hold the band-32 tiling)
+  auto flush = [&](int b) {
+    const int c = b + (lane & 15);
+    double* wcol = win + (c % WIN) * STRIDE;
+    const bool in = c < width;
+    const int rh = (lane >> 4) * 16;
+#pragma unroll 8
+    for (int j = 0; j < 16; ++j) {
+      const int row = rh + j;
+      const int64_t off = __shfl_sync(0xffffffffu, fout, row);
+      const double sc = __shfl_sync(0xffffffffu, fscale, row);
+      if (off >= 0 && in) a.A[off + col0 + c] = wcol[row] * sc;
+      wcol[row] = 0.0;
+    }
+    __syncwarp();
+  };
+
+  for (int p = 0; p < ns; ++p) {
+    const int s = p % S;
+    sweep::mbar_wait(full + s, (unsigned)(p / S) & 1u);
+    const double* pr = ring + s * (R * REC);
+    const int mfirst = reinterpret_cast<const int*>(pr + RC::TAIL + 6)[1];
+    while (mfirst >= base + FLUSH) {
+      flush(base);
+      base += FLUSH;
+    }
+    // per record: x' = x - cc (IEEE, also the classification's difference)
+    d3 xc[R];
+    double sq[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const double* tl = pr + j * REC + RC::TAIL;
+      xc[j] = sub_rn(X0, mk3(tl[0], tl[1], tl[2]));
+      sq[j] = fma(xc[j].z, xc[j].z, fma(xc[j].y, xc[j].y, xc[j].x * xc[j].x));
+    }
+    double acc[R][3];
+#pragma unroll
+    for (int j = 0; j < R; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
+    if (MODE == 0) {
+#pragma unroll
+      for (int q = 0; q < RC::NQP; q += 2) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const double* nd = pr + j * REC + 5 * q;
+          const double2 y01 = *reinterpret_cast<const double2*>(nd);
+          const double2 y2p = *reinterpret_cast<const double2*>(nd + 2);
+          const double2 qq = *reinterpret_cast<const double2*>(nd + 4);
+          const double2 z01 = *reinterpret_cast<const double2*>(nd + 6);
+          const double2 z2p = *reinterpret_cast<const double2*>(nd + 8);
+          const double r0 = fma(xc[j].x, y01.x, fma(xc[j].y, y01.y, fma(xc[j].z, y2p.x, fma(sq[j], qq.x, y2p.y))));
+          const double r1 = fma(xc[j].x, z01.x, fma(xc[j].y, z01.y, fma(xc[j].z, z2p.x, fma(sq[j], qq.y, z2p.y))));
+          const double k0 = rsqrt2_newton(r0);
+          const double k1 = rsqrt2_newton(r1);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            acc[j][c] = fma(k0, a.hats[q][c], acc[j][c]);
+            acc[j][c] = fma(k1, a.hats[q + 1][c], acc[j][c]);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const double* rec = pr + j * REC;
+          const double2 p01 = *reinterpret_cast<const double2*>(rec + 6 * q);
+          const double2 p2w = *reinterpret_cast<const double2*>(rec + 6 * q + 2);
+          const double2 w12 = *reinterpret_cast<const double2*>(rec + 6 * q + 4);
+          const double dx = X0.x - p01.x, dy = X0.y - p01.y, dz = X0.z - p2w.x;
+          const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+          const double ri = rsqrt_full(r2);
+          const double dn = fma(dz, N0.z, fma(dy, N0.y, dx * N0.x));
+          const double k = dn * (ri * ri * ri);
+          acc[j][0] = fma(k, p2w.y, acc[j][0]);
+          acc[j][1] = fma(k, w12.x, acc[j][1]);
+          acc[j][2] = fma(k, w12.y, acc[j][2]);
+        }
+      }
+    }
+    int slots[R][3];
+    bool emit[R];
+    int tris[R];
+    bool any_emit = false;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const double* tl = pr + j * REC + RC::TAIL;
+      const bool valid = R * p + j < ne;
+      const bool reg = sweep::regular(xc[j], sq[j], tl);
+      if (!reg) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
+      const int* meta = reinterpret_cast<const int*>(tl + 6);
+      const unsigned sl = static_cast<unsigned>(meta[2]), sf = static_cast<unsigned>(meta[3]);
+      slots[j][0] = valid ? (int)(sl & 0xffffu) : WIN;
+      slots[j][1] = valid ? (int)(sl >> 16) : WIN;
+      slots[j][2] = valid ? (int)(sf & 0xffffu) : WIN;
+      const bool prim = valid && (sf >> 16) & 1u;
+      tris[j] = valid ? meta[0] : 0;
+      emit[j] = !reg && prim && live0;
+      any_emit |= emit[j];
+    }
+    __syncwarp();
+    // this warp is done reading the stage: the last warp to release it
+    // refills it with stage p + S
+    if (lane == 0) {
+      unsigned old;
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(old)
+                   : "r"(sweep::smem_u32(released + s))
+                   : "memory");
+      if (old == (unsigned)live_warps - 1u) {
+        released[s] = 0;
+        if (p + S < ns) issue(p + S);
+      }
+    }
+    // deferred near pairs (rare): emitted from the panel's primary tile only
+    if (__any_sync(0xffffffffu, any_emit)) {
+      unsigned msk[R];
+      int total = 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int* tc = a.tri_cols + 3 * (size_t)tris[j];
+        emit[j] = emit[j] && !(tc[0] == own0 || tc[1] == own0 || tc[2] == own0);
+        msk[j] = __ballot_sync(0xffffffffu, emit[j]);
+        total += __popc(msk[j]);
+      }
+      unsigned long long b = 0;
+      if (lane == 0 && total) b = atomicAdd(a.near_count, (unsigned long long)total);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      const unsigned lt = (1u << lane) - 1u;
+      long long off = (long long)b;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        if (emit[j]) {
+          const long long slot = off + __popc(msk[j] & lt);
+          if (slot < a.near_cap) {
+            a.near_list[2 * slot] = a.row_begin + i0;
+            a.near_list[2 * slot + 1] = tris[j];
+          }
+        }
+        off += __popc(msk[j]);
+      }
+    }
+    // window adds in record order (each lane owns its row: no conflicts)
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      win[slots[j][0] * STRIDE + lane] += acc[j][0];
+      win[slots[j][1] * STRIDE + lane] += acc[j][1];
+      win[slots[j][2] * STRIDE + lane] += acc[j][2];
+    }
+    __syncwarp();
+  }
+  while (base < width) {
+    flush(base);
+    base += FLUSH;
+  }
+}
+
+template <int NQ, int MODE>
+static cudaError_t launch_sweep_nq(const RegularArgs& a, cudaStream_t st) {
+  using namespace sweep;
+  const size_t smem = (size_t)(2 * S + S * R * Rec<NQ, MODE>::DOUBLES + WPC * WREG) * sizeof(double);
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(k_sweep<NQ, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  dim3 grid((a.n_rows + ROWS * WPC - 1) / (ROWS * WPC), a.n_tiles);
+  k_sweep<NQ, MODE><<<grid, 32 * WPC, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+int sweep_record_doubles(int nq, int mode) {
+  switch (nq) {
+    case 3: return mode == 0 ? sweep::Rec<3, 0>::DOUBLES : sweep::Rec<3, 1>::DOUBLES;
+    case 6: return mode == 0 ? sweep::Rec<6, 0>::DOUBLES : sweep::Rec<6, 1>::DOUBLES;
+    case 12: return mode == 0 ? sweep::Rec<12, 0>::DOUBLES : sweep::Rec<12, 1>::DOUBLES;
+    case 16: return mode == 0 ? sweep::Rec<16, 0>::DOUBLES : sweep::Rec<16, 1>::DOUBLES;
+  }
+  return -1;
+}
+
+// mode 0: SL rows (SL record stream), 1: ADL rows (ADL record stream)
+cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, cudaStream_t st) {
+  if (a.n_rows <= 0 || a.n_tiles <= 0) return cudaSuccess;
+  auto go = [&](auto nq_tag) -> cudaError_t {
+    constexpr int Q = decltype(nq_tag)::value;
+    return mode == 0 ? launch_sweep_nq<Q, 0>(a, st) : launch_sweep_nq<Q, 1>(a, st);
+  };
+  switch (nq) {
+    case 3: return go(std::integral_constant<int, 3>{});
+    case 6: return go(std::integral_constant<int, 6>{});
+    case 12: return go(std::integral_constant<int, 12>{});
+    case 16: return go(std::integral_constant<int, 16>{});
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hvb

@@ -89,79 +89,30 @@ __global__ void __launch_bounds__(GEMV_THREADS) k_gemv_f64(const double* __restr
   }
 }
 
-template <int ROWS>
-__global__ void __launch_bounds__(GEMV_THREADS) k_gemv_f32(const float* __restrict__ A, int64_t lda, int nrows,
-                                                           int ncols, const double* __restrict__ x,
-                                                           const double* __restrict__ left,
-                                                           double* __restrict__ y) {
-  // single-precision storage (reference casts v to float32 and reduces in
-  // float32, src/assembly.py:388); we keep float32 products but reduce in
-  // float64 -- at least as accurate, documented in DESIGN.md.
-  const int r0 = blockIdx.x * ROWS;
-  const int tid = threadIdx.x;
-  double acc[ROWS];
-#pragma unroll
-  for (int r = 0; r < ROWS; ++r) acc[r] = 0.0;
-  const int n4 = ncols >> 2;
-  const float4* rowp[ROWS];
-#pragma unroll
-  for (int r = 0; r < ROWS; ++r) {
-    int rr = min(r0 + r, nrows - 1);
-    rowp[r] = reinterpret_cast<const float4*>(A + (int64_t)rr * lda);
-  }
-  for (int k = tid; k < n4; k += GEMV_THREADS) {
-    const float x0 = (float)x[4 * k], x1 = (float)x[4 * k + 1], x2 = (float)x[4 * k + 2], x3 = (float)x[4 * k + 3];
-#pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-      float4 a = __ldcs(rowp[r] + k);
-      acc[r] += (double)(a.x * x0) + (double)(a.y * x1) + (double)(a.z * x2) + (double)(a.w * x3);
-    }
-  }
-  if (tid == 0) {
-    for (int c = n4 * 4; c < ncols; ++c) {
-      const float xv = (float)x[c];
-#pragma unroll
-      for (int r = 0; r < ROWS; ++r) {
-        int rr = min(r0 + r, nrows - 1);
-        acc[r] += (double)(A[(int64_t)rr * lda + c] * xv);
-      }
-    }
-  }
-  __shared__ double red[ROWS][GEMV_THREADS / 32];
-  const int lane = tid & 31, wid = tid >> 5;
-#pragma unroll
-  for (int r = 0; r < ROWS; ++r) {
-    double v = warp_sum(acc[r]);
-    if (lane == 0) red[r][wid] = v;
-  }
-  __syncthreads();
-  if (tid < ROWS && r0 + tid < nrows) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < GEMV_THREADS / 32; ++w) s += red[tid][w];
-    y[r0 + tid] = left ? left[r0 + tid] * s : s;
-  }
-}
-
-// Single-precision storage with 256-bit loads (8 floats per load): float32
-// partial sums over 8 columns (the reference reduces in float32,
-// src/assembly.py:388), accumulated in float64 across chunks; 2 rows per CTA.
+// Single-precision storage (reference matvec src/assembly.py:386-392: v is
+// cast to float32 and every row is reduced by a float32 dot, data[i] @ vc).
+// 256-bit loads (8 floats), 8 rows per CTA.  F32ACC (the reference
+// semantics, default): products and every partial sum in float32 (FMA
+// chains per thread, then a float32 tree over the CTA), the row result
+// widened to double at the end.  !F32ACC (opt-in, hvb_gemv prec 2): float32
+// partials over 8 columns accumulated in double.
 HVB_DEV void ld256f(const float* p, float* v) {
   asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
                : "l"(p));
 }
 
-template <int ROWS>
+template <int ROWS, bool F32ACC>
 __global__ void __launch_bounds__(GEMV_THREADS) k_gemv_f32_v8(const float* __restrict__ A, int64_t lda, int nrows,
                                                               int ncols, const double* __restrict__ x,
                                                               const double* __restrict__ left,
                                                               double* __restrict__ y) {
+  using Acc = typename std::conditional<F32ACC, float, double>::type;
   const int r0 = blockIdx.x * ROWS;
   const int tid = threadIdx.x;
-  double acc[ROWS];
+  Acc acc[ROWS];
 #pragma unroll
-  for (int r = 0; r < ROWS; ++r) acc[r] = 0.0;
+  for (int r = 0; r < ROWS; ++r) acc[r] = Acc(0);
   const int n8 = ncols >> 3;
   const float* rowp[ROWS];
 #pragma unroll
@@ -174,32 +125,44 @@ __global__ void __launch_bounds__(GEMV_THREADS) k_gemv_f32_v8(const float* __res
     for (int r = 0; r < ROWS; ++r) {
       float a[8];
       ld256f(rowp[r] + 8 * k, a);
-      float s = a[0] * xf[0];  // float partial over 8 columns (the reference reduces in float32)
+      if (F32ACC) {
+        float s = (float)acc[r];
 #pragma unroll
-      for (int j = 1; j < 8; ++j) s = fmaf(a[j], xf[j], s);
-      acc[r] += (double)s;
+        for (int j = 0; j < 8; ++j) s = fmaf(a[j], xf[j], s);
+        acc[r] = s;
+      } else {
+        float s = a[0] * xf[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) s = fmaf(a[j], xf[j], s);
+        acc[r] += (double)s;
+      }
     }
   }
   if (tid == 0) {
     for (int c = 8 * n8; c < ncols; ++c) {
       const float xv = (float)x[c];
 #pragma unroll
-      for (int r = 0; r < ROWS; ++r) acc[r] += (double)(rowp[r][c] * xv);
+      for (int r = 0; r < ROWS; ++r) {
+        if (F32ACC)
+          acc[r] = fmaf(rowp[r][c], xv, (float)acc[r]);
+        else
+          acc[r] += (double)(rowp[r][c] * xv);
+      }
     }
   }
-  __shared__ double red[ROWS][GEMV_THREADS / 32];
+  __shared__ Acc red[ROWS][GEMV_THREADS / 32];
   const int lane = tid & 31, wid = tid >> 5;
 #pragma unroll
   for (int r = 0; r < ROWS; ++r) {
-    double v = warp_sum(acc[r]);
+    Acc v = warp_sum(acc[r]);
     if (lane == 0) red[r][wid] = v;
   }
   __syncthreads();
   if (tid < ROWS && r0 + tid < nrows) {
-    double s = 0.0;
+    Acc s = Acc(0);
 #pragma unroll
     for (int w = 0; w < GEMV_THREADS / 32; ++w) s += red[tid][w];
-    y[r0 + tid] = left ? left[r0 + tid] * s : s;
+    y[r0 + tid] = left ? left[r0 + tid] * (double)s : (double)s;
   }
 }
 
@@ -256,14 +219,18 @@ static bool v4_ok(const void* A, int64_t lda, const double* x) {
   return lda % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 31) == 0 && (reinterpret_cast<uintptr_t>(x) & 31) == 0;
 }
 
-cudaError_t launch_gemv(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const double* x,
+// prec 0: double matrix; 1: float matrix, float32 reduction (reference
+// semantics); 2: float matrix, float32 partials accumulated in double
+cudaError_t launch_gemv(const void* A, int prec, int64_t lda, int nrows, int ncols, const double* x,
                         const double* left, double* y, cudaStream_t st) {
   if (nrows == 0) return cudaSuccess;
-  if (is_f32 && lda % 8 == 0 && (reinterpret_cast<uintptr_t>(A) & 31) == 0) {
-    k_gemv_f32_v8<8><<<(nrows + 7) / 8, GEMV_THREADS, 0, st>>>((const float*)A, lda, nrows, ncols, x, left, y);
-  } else if (is_f32) {
-    constexpr int R = 8;
-    k_gemv_f32<R><<<(nrows + R - 1) / R, GEMV_THREADS, 0, st>>>((const float*)A, lda, nrows, ncols, x, left, y);
+  if (prec != 0) {
+    if (lda % 8 != 0 || (reinterpret_cast<uintptr_t>(A) & 31) != 0) return cudaErrorInvalidValue;
+    if (prec == 1)
+      k_gemv_f32_v8<8, true><<<(nrows + 7) / 8, GEMV_THREADS, 0, st>>>((const float*)A, lda, nrows, ncols, x, left, y);
+    else
+      k_gemv_f32_v8<8, false><<<(nrows + 7) / 8, GEMV_THREADS, 0, st>>>((const float*)A, lda, nrows, ncols, x, left,
+                                                                        y);
   } else if (v4_ok(A, lda, x)) {
     k_gemv_f64_v4<2><<<(nrows + 1) / 2, GEMV_THREADS, 0, st>>>((const double*)A, lda, nrows, ncols, x, left, y,
                                                                nullptr, 0, 0);
@@ -599,25 +566,5 @@ __global__ void k_gemv_f64_v4(const double* __restrict__ A, int64_t lda, int nro
   }
 }
 
-cudaError_t launch_gemv_variant(const double* A, int64_t lda, int nrows, int ncols, const double* x, double* y,
-                                int variant, cudaStream_t st) {
-  switch (variant) {
-    case 0: k_gemv_f64<8><<<(nrows + 7) / 8, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
-    case 1: k_gemv_f64_v4<8><<<(nrows + 7) / 8, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
-    case 2: k_gemv_f64_v4<4><<<(nrows + 3) / 4, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
-    case 3: k_gemv_f64_v4<16><<<(nrows + 15) / 16, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
-    case 4: k_gemv_f64<4><<<(nrows + 3) / 4, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
-    case 5: k_gemv_f64<16><<<(nrows + 15) / 16, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
-    case 6: k_gemv_f64_v4<2><<<(nrows + 1) / 2, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
-    case 7: k_gemv_f64_v4<1><<<nrows, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, nullptr, y, nullptr, 0, 0); break;
-    default: return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
-}
-
 }  // namespace hvb
 
-extern "C" int hvb_bench_gemv(const double* A, long long lda, int nrows, int ncols, const double* x, double* y,
-                              int variant, void* stream) {
-  return hvb::launch_gemv_variant(A, lda, nrows, ncols, x, y, variant, (cudaStream_t)stream) == cudaSuccess ? 0 : 2;
-}

@@ -47,31 +47,28 @@ int hvb_panel_data(const double* circumcenters, const double* radii, int nt, dou
 }
 
 int hvb_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
-                     const int* ent_meta, long long n_entries, int centered, int window, double* stream_out,
+                     const int* ent_meta, long long n_entries, int mode, int window, double* stream_out,
                      void* stream) {
   if (n_entries < 0) return fail(HVB_EARG, "hvb_build_stream: negative entry count");
+  if (mode != 0 && mode != 1) return fail(HVB_EARG, "hvb_build_stream: mode must be 0 (SL) or 1 (ADL)");
   if (window < 1 || window > 32767) return fail(HVB_EARG, "hvb_build_stream: window out of range");
-  return check(hvb::launch_build_stream(table, nq, ccr, eta, ent_tri, ent_meta, n_entries, centered, window,
+  if (hvb::sweep_record_doubles(nq, mode) < 0) return fail(HVB_EARG, "hvb_build_stream: nq must be 3, 6, 12 or 16");
+  return check(hvb::launch_build_stream(table, nq, ccr, eta, ent_tri, ent_meta, n_entries, mode, window,
                                         stream_out, (cudaStream_t)stream),
                "hvb_build_stream");
 }
 
+int hvb_stream_record_doubles(int nq, int mode) { return hvb::sweep_record_doubles(nq, mode); }
+
 int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_col0,
-                         const int* tile_width, int n_tiles, int nq, int row_begin, int n_rows, const double* rowdata,
-                         const int* row_kind, const int* row_col, const double* row_scale,
-                         const long long* row_out, double* A, const int* tri_cols, int mode, int warps_per_block,
+                         const int* tile_width, int n_tiles, int nq, const double* hats, int row_begin, int n_rows,
+                         const double* rowdata, const int* row_col, const double* row_scale,
+                         const long long* row_out, double* A, const int* tri_cols, int mode,
                          int* near_list, unsigned long long* near_count, long long near_cap, void* stream) {
   if (n_rows <= 0 || n_tiles <= 0) return HVB_OK;
-  // window columns: bits 8-15 if set (row4: 40/48/56/64), else bit 2 -> 64, else 96
-  const int window = ((mode >> 8) & 0xff) ? (mode >> 8) & 0xff : (mode & 4) ? 64 : 96;
-  const int rpl = (mode >> 16) & 0xf;
-  const bool flush16 = (mode >> 20) & 1;  // bit 20: row layouts flush 16 columns at a time (band <= window - 16)  // row layouts: records per lane per step (bits 16-19; 0 = layout default)
-  const bool quad = (mode & 8) != 0;        // bit 3: quad layout (tiling band over groups of 4 records)
-  const bool row4 = (mode & 16) != 0;       // bit 4: row4 layout (same tiling as quad)
-  const bool row8 = (mode & 32) != 0;       // bit 5: row8 layout (band over groups of 8 records)
-  mode &= 3;
-  if (mode > 2 || warps_per_block < 1 || warps_per_block > 8)
-    return fail(HVB_EARG, "hvb_assemble_regular: bad mode / warps_per_block");
+  if (mode != 0 && mode != 1) return fail(HVB_EARG, "hvb_assemble_regular: mode must be 0 (SL) or 1 (ADL)");
+  if (hvb::sweep_record_doubles(nq, mode) < 0) return fail(HVB_EARG, "hvb_assemble_regular: nq must be 3, 6, 12 or 16");
+  if (mode == 0 && !hats) return fail(HVB_EARG, "hvb_assemble_regular: the SL sweep needs the hat table");
   hvb::RegularArgs a;
   std::memset(&a, 0, sizeof a);
   a.stream = panel_stream;
@@ -82,7 +79,6 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
   a.row_begin = row_begin;
   a.n_rows = n_rows;
   a.rowdata = rowdata;
-  a.row_kind = row_kind;
   a.row_col = row_col;
   a.row_scale = row_scale;
   a.row_out = (const int64_t*)row_out;
@@ -91,14 +87,10 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
   a.near_list = near_list;
   a.near_count = near_count;
   a.near_cap = near_cap;
-  if (row4 || row8)
-    return check(hvb::launch_regular_row4(a, nq, mode, window, (rpl ? rpl : row8 ? 8 : 4), flush16 ? 16 : 32,
-                                          (cudaStream_t)stream),
-                 "hvb_assemble_regular");
-  if (quad)
-    return check(hvb::launch_regular_quad(a, nq, mode, window, (cudaStream_t)stream), "hvb_assemble_regular");
-  return check(hvb::launch_regular(a, nq, mode, window, warps_per_block, (cudaStream_t)stream),
-               "hvb_assemble_regular");
+  if (hats)
+    for (int q = 0; q < nq; ++q)
+      for (int c = 0; c < 3; ++c) a.hats[q][c] = hats[3 * q + c];
+  return check(hvb::launch_regular(a, nq, mode, (cudaStream_t)stream), "hvb_assemble_regular");
 }
 
 int hvb_assemble_singular(const double* nodes6, const int* tri_cols, const int* col_dev, const int* vc_ptr,
@@ -162,10 +154,12 @@ int hvb_near_apply_rows(const int* seg_ptr, int n_seg, const int* pairs, const d
                "hvb_near_apply_rows");
 }
 
-int hvb_gemv(const void* A, int is_f32, long long lda, int n_rows, int n_cols, const double* x, const double* left,
+int hvb_gemv(const void* A, int prec, long long lda, int n_rows, int n_cols, const double* x, const double* left,
              double* y, void* stream) {
   if (lda < n_cols || (lda % 4) != 0) return fail(HVB_EARG, "hvb_gemv: lda must be >= n_cols and a multiple of 4");
-  return check(hvb::launch_gemv(A, is_f32, lda, n_rows, n_cols, x, left, y, (cudaStream_t)stream), "hvb_gemv");
+  if (prec < 0 || prec > 2) return fail(HVB_EARG, "hvb_gemv: prec must be 0 (f64), 1 (f32) or 2 (f32, f64 sums)");
+  if (prec != 0 && (lda % 8) != 0) return fail(HVB_EARG, "hvb_gemv: float32 storage needs lda % 8 == 0");
+  return check(hvb::launch_gemv(A, prec, lda, n_rows, n_cols, x, left, y, (cudaStream_t)stream), "hvb_gemv");
 }
 
 int hvb_gemv_bcast(const double* A, long long lda, int n_rows, int n_cols, const double* x, const double* left,

@@ -8,7 +8,7 @@
 namespace hvb {
 
 struct RegularArgs {
-  const double* stream;     // tile panel streams, records of REC doubles
+  const double* stream;     // tile panel streams (csrc/assemble.cu record formats)
   const int64_t* tile_ptr;  // (n_tiles+1) record offsets
   const int* tile_col0;     // first device column of each tile
   const int* tile_width;    // owned columns of each tile
@@ -16,7 +16,6 @@ struct RegularArgs {
   int row_begin;            // first row-list entry of this launch
   int n_rows;               // rows in this launch
   const double* rowdata;    // RowData per row-list entry (6 doubles)
-  const int* row_kind;      // 0 SL, 1 ADL  (per row-list entry)
   const int* row_col;       // own collocation column (singular test), -1 none
   const double* row_scale;  // multiplies every entry of the row
   const int64_t* row_out;   // output row offset (in elements) into A
@@ -25,6 +24,7 @@ struct RegularArgs {
   int* near_list;           // (cap, 2): (row-list index, triangle)
   unsigned long long* near_count;
   long long near_cap;
+  double hats[16][3];       // hat_c(q) of the regular rule (SL stream; zero past nq)
 };
 
 struct SingularArgs {
@@ -82,14 +82,12 @@ struct FieldArgs {
   double* out;            // (m, 3) reduced field (dynamic path)
 };
 
-cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, int window, int wpb, cudaStream_t st);
-cudaError_t launch_regular_quad(const RegularArgs& a, int nq, int mode, int window, cudaStream_t st);
-cudaError_t launch_regular_row4(const RegularArgs& a, int nq, int mode, int window, int r, int flush,
-                                cudaStream_t st);
+cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, cudaStream_t st);
+int sweep_record_doubles(int nq, int mode);
 cudaError_t launch_build_table(const double* nodes6, int nt, int nq, const double* rule, double* out,
                                cudaStream_t st);
 cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,
-                                const int* ent_meta, int64_t ne, int centered, int window, double* out,
+                                const int* ent_meta, int64_t ne, int mode, int window, double* out,
                                 cudaStream_t st);
 cudaError_t launch_panel_data(const double* cc, const double* radii, int nt, double eta, double* ccr, double* cls,
                               double* groups, cudaStream_t st);
@@ -100,7 +98,7 @@ cudaError_t launch_near_pairs(const NearArgs& a, cudaStream_t st);
 cudaError_t launch_near_apply_rows(const int* seg_ptr, int n_seg, const int* pairs, const double* contrib,
                                    const int* tri_cols, const int* col_dev, const double* row_scale,
                                    const int64_t* row_out, double* A, cudaStream_t st);
-cudaError_t launch_gemv(const void* A, int is_f32, int64_t lda, int nrows, int ncols, const double* x,
+cudaError_t launch_gemv(const void* A, int prec, int64_t lda, int nrows, int ncols, const double* x,
                         const double* left, double* y, cudaStream_t st);
 cudaError_t launch_gemv_bcast(const double* A, int64_t lda, int nrows, int ncols, const double* x, const double* left,
                               double* const* outs, int n_out, int64_t out_off, cudaStream_t st);

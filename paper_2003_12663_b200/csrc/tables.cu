@@ -1,7 +1,6 @@
 // Assembly support kernels: regular-rule sample table (K1), panel-stream
 // packing, the singular Duffy pass (K4) and the floating columns (K6).  The
-// regular sweep itself is csrc/assemble_row4.cu (csrc/assemble_quad.cu and
-// csrc/assemble_dual.cu are the measured alternatives).
+// regular sweep itself is csrc/assemble.cu.
 //
 // Reference: TriangleTables src/assembly.py:73-118, row_pass1 singular batch
 // 202-235, _row_equation 408-468.
@@ -83,48 +82,52 @@ __global__ void k_panel_data(const double* __restrict__ cc, const double* __rest
   }
 }
 
-// Pack one stream record per (tile, panel) entry.
-// centered = 0: per node (y, w0, w1, w2) -- 6 doubles (dual / quad layouts).
-// centered = 1: per node (-2 (y - cc), |y - cc|^2, w0, w1, w2, 0) -- 8 doubles
-// relative to the panel's circumcentre cc (measured for the row4 layout,
-// slower there -- device.py CENTERED): a kernel can then
-// forms r^2 = |x-cc|^2 + |y-cc|^2 - 2 (x-cc).(y-cc) in 4 FP64 ops, with the
-// |x-cc|^2 it already needs for the classification.  Regular pairs have
-// |x-cc| > 1.2 R >= |y-cc| + 0.2 R, so the cancellation costs at most ~100 ulp
-// of r^2 (1e-14 relative).  The record tail (8 doubles) follows the nodes.
+// Pack one stream record per (tile, panel) entry (record formats: see
+// csrc/assemble.cu).  mode 0 = SL stream: per node q of panel t, with
+// w = jw/(4 pi) (the table's three weights summed), s = 1/w^2 and
+// y' = y - cc (IEEE):  Y = -2 s y', P = s |y'|^2, Q = s, stored per node
+// pair as [Y0x Y0y | Y0z P0 | Q0 Q1 | Y1x Y1y | Y1z P1]; an odd nq is padded
+// with a node (Y = 0, P = 1, Q = 0) whose hat values are zero.  mode 1 = ADL
+// stream: the table's (y, w hat_0, w hat_1, w hat_2) per node.
 __global__ void k_build_stream(const double* __restrict__ table, int nq,
                                const double* __restrict__ ccr,  // (nt,4): cc, R
                                double eta, const int* __restrict__ ent_tri,
                                const int* __restrict__ ent_meta,  // (ne,5): mfirst, slot0, slot1, slot2, flags
-                               int64_t ne, int centered, int window, double* __restrict__ out) {
+                               int64_t ne, int mode, int rec, int window, double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= ne) return;
-  const int per = centered ? 8 : 6;
-  const int rec = per * nq + 8;
   int t = ent_tri[e];
   double* o = out + e * rec;
   const double* s = table + (size_t)t * 6 * nq;
   const double* c = ccr + 4 * (size_t)t;
-  if (centered) {
-    for (int q = 0; q < nq; ++q) {
-      const double* y = s + 6 * q;
-      const d3 yc = sub_rn(mk3(y[0], y[1], y[2]), mk3(c[0], c[1], c[2]));
-      double* oq = o + 8 * q;
-      oq[0] = -2.0 * yc.x;
-      oq[1] = -2.0 * yc.y;
-      oq[2] = -2.0 * yc.z;
-      oq[3] = sumsq_unfused(yc);
-      oq[4] = y[3];
-      oq[5] = y[4];
-      oq[6] = y[5];
-      oq[7] = 0.0;
+  if (mode == 0) {
+    const int nqp = (nq + 1) & ~1;
+    for (int q = 0; q < nqp; ++q) {
+      double Y[3] = {0.0, 0.0, 0.0}, P = 1.0, Q = 0.0;
+      if (q < nq) {
+        const double* y = s + 6 * q;
+        const d3 yc = sub_rn(mk3(y[0], y[1], y[2]), mk3(c[0], c[1], c[2]));
+        const double w = (y[3] + y[4]) + y[5];
+        const double sc = 1.0 / (w * w);
+        Y[0] = -2.0 * sc * yc.x;
+        Y[1] = -2.0 * sc * yc.y;
+        Y[2] = -2.0 * sc * yc.z;
+        P = sc * sumsq_unfused(yc);
+        Q = sc;
+      }
+      double* op = o + 10 * (q >> 1);
+      if ((q & 1) == 0) {
+        op[0] = Y[0]; op[1] = Y[1]; op[2] = Y[2]; op[3] = P; op[4] = Q;
+      } else {
+        op[5] = Q; op[6] = Y[0]; op[7] = Y[1]; op[8] = Y[2]; op[9] = P;
+      }
     }
   } else {
     for (int k = 0; k < 6 * nq; ++k) o[k] = s[k];
   }
   double thr = __dmul_rn(eta, c[3]);
   double t2 = thr * thr;
-  double* tail = o + per * nq;
+  double* tail = o + rec - 8;
   tail[0] = c[0];
   tail[1] = c[1];
   tail[2] = c[2];
@@ -225,10 +228,12 @@ cudaError_t launch_panel_data(const double* cc, const double* radii, int nt, dou
 }
 
 cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, double eta,
-                                const int* ent_tri, const int* ent_meta, int64_t ne, int centered, int window,
+                                const int* ent_tri, const int* ent_meta, int64_t ne, int mode, int window,
                                 double* out, cudaStream_t st) {
   if (ne == 0) return cudaSuccess;
-  k_build_stream<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(table, nq, ccr, eta, ent_tri, ent_meta, ne, centered,
+  const int rec = sweep_record_doubles(nq, mode);
+  if (rec < 0) return cudaErrorInvalidValue;
+  k_build_stream<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(table, nq, ccr, eta, ent_tri, ent_meta, ne, mode, rec,
                                                               window, out);
   return cudaGetLastError();
 }

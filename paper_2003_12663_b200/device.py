@@ -9,7 +9,7 @@ Host side (NumPy, once per mesh):
   corners of every aligned group of GROUP consecutive records lie within
   ``band`` columns of the group's first owned column, which is what lets
   the assembly warp keep a WINDOW-column sliding window of running sums
-  (csrc/assemble_row4.cu: WINDOW 48, flushes of 16 columns, band 32).
+  (csrc/assemble.cu: WINDOW 48, flushes of 16 columns, band 32).
   Panels with corners in several tiles are evaluated once per tile
   (``redundancy``, 1.14 at config 4).
 * entries (tile, panel) sorted by (tile, first owned column).
@@ -31,37 +31,16 @@ import numpy as np
 from . import _lib
 from .quadrature import QuadConfig, duffy_rule, graded_rule, regular_rule
 
-__all__ = ["ColumnTiling", "column_tiling", "DeviceMesh", "device_mesh", "WINDOW_BAND"]
+__all__ = ["ColumnTiling", "column_tiling", "DeviceMesh", "device_mesh", "WINDOW"]
 
-WINDOW_BAND = 64  # default band of column_tiling (dual layout, 96-column window)
-# regular-sweep window (row4: 40/48/56/64 columns, dual/quad: 64/96) and tile
-# shape; env overrides are for A/B measurements (tools/ab.sh).  Measured on
-# cfg4 (regular kernel): row4 x 48 columns 0.319 s, x 56 0.336, x 64 0.346,
-# x 40 0.360 (the window's shared memory sets the resident warps; a narrower
-# window means more tile-boundary panels: redundancy 1.14 at 64, 1.21 at 48)
-WINDOW = int(os.environ.get("HVB_ASM_WIN", "0"))  # 0: 48 for row4 (best on cfg4), else 64
-STRIPS = os.environ.get("HVB_ASM_STRIPS", "1") == "1"
-# quad layout (csrc/assemble_quad.cu: 2 records x 2 rows per lane) needs the
-# band bounded over groups of 4 records; the dual layout over groups of 2
-# row4 layout (csrc/assemble_row4.cu: lane = row, 4 records per lane) uses
-# the same stream as quad
-LAYOUT = os.environ.get("HVB_ASM_LAYOUT", "row4")
-QUAD = LAYOUT in ("quad", "row4", "row8")
-RPL = int(os.environ.get("HVB_ASM_R", "0"))  # row layouts: records per lane (0 = default)
-GROUP = RPL if RPL and LAYOUT == "row4" else {"dual": 2, "quad": 4, "row4": 4, "row8": 8}[LAYOUT]
-LAYOUT_BITS = {"dual": 0, "quad": 8, "row4": 16, "row8": 32}[LAYOUT] | ((RPL << 16) if LAYOUT == "row4" else 0)
-WINDOW = WINDOW or (48 if LAYOUT == "row4" else 64)
-# row4 flushes 16 finished columns at a time, so a WINDOW-column window holds
-# a band of WINDOW - 16 (else WINDOW - 32)
-FLUSH = int(os.environ.get("HVB_ASM_FLUSH", "16")) if LAYOUT == "row4" else 32
-if FLUSH == 16:
-    LAYOUT_BITS |= 1 << 20
-# circumcentre-centred panel records (csrc/tables.cu, centered = 1) save two
-# FP64 ops per node-row but need 8 doubles per node: the bigger ring drops
-# row4 to 9 resident warps/SM and it measured slower (0.365 vs 0.343 s on
-# cfg4), so every layout reads the plain 6-double records
-CENTERED = False
-MAX_TILE = int(os.environ.get("HVB_ASM_MAXTILE", "32767"))
+# regular-sweep geometry (csrc/assemble.cu): a 48-column window per warp,
+# flushed 16 columns at a time, so the panel band over every aligned group of
+# GROUP = 4 records (one bulk-copy stage) must stay within WINDOW - FLUSH = 32
+# columns.  Measured on cfg4 in round 1: 48 columns beat 40/44/56/64.
+WINDOW = 48
+FLUSH = 16
+GROUP = 4
+MAX_TILE = 32767
 
 
 @dataclass
@@ -132,7 +111,7 @@ def _split_across(points: np.ndarray, tile: np.ndarray):
 
 
 def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = 2048,
-                  band_max: int = WINDOW_BAND, group: int = 2, strips: bool = False) -> ColumnTiling:
+                  band_max: int = WINDOW - FLUSH, group: int = GROUP, strips: bool = False) -> ColumnTiling:
     """Column tiles + sorted (tile, panel) entries.  The band is measured
     over groups of ``group`` consecutive records of each tile (starting at
     the tile's first record), as the grouped assembly kernel keeps a whole
@@ -260,24 +239,40 @@ class DeviceMesh:
 
         # column tiling + panel streams
         self.window = WINDOW
-        tiling = mesh_tiling(mesh, max_tile, WINDOW, STRIPS, GROUP, FLUSH)
-        self.layout_bits = LAYOUT_BITS
+        tiling = mesh_tiling(mesh, max_tile, WINDOW, True, GROUP, FLUSH)
         self.tiling = tiling
         self.perm = up(tiling.perm, **i32)
         self.col_dev = up(tiling.inv, **i32)
         self.tile_ptr = up(tiling.tile_ptr, dtype=torch.int64, device=device)
         self.tile_col0 = up(tiling.tile_col0, **i32)
         self.tile_width = up(tiling.tile_width, **i32)
-        ent_tri = up(tiling.ent_tri, **i32)
-        ent_meta = up(tiling.ent_meta, **i32)  # (mfirst, l0, l1, l2, flags); slots = l % WINDOW on the device
-        ne = len(tiling.ent_tri)
-        self.centered = CENTERED
-        self.rec = (8 if CENTERED else 6) * self.nq + 8
-        self.stream = torch.empty((ne, self.rec), **f64)
-        _lib.call("hvb_build_stream", _lib.ptr(self.table), self.nq, _lib.ptr(self.ccr), float(cfg.eta),
-                  _lib.ptr(ent_tri), _lib.ptr(ent_meta), ne, int(CENTERED), WINDOW, _lib.ptr(self.stream), st)
+        self._ent_tri = up(tiling.ent_tri, **i32)
+        self._ent_meta = up(tiling.ent_meta, **i32)  # (mfirst, l0, l1, l2, flags); slots = l % WINDOW on the device
+        self.n_entries = len(tiling.ent_tri)
+        self.hats = np.ascontiguousarray(
+            np.column_stack([1.0 - reg.nodes[:, 0] - reg.nodes[:, 1], reg.nodes[:, 0], reg.nodes[:, 1]]))
+        self._streams = {}
+        self.stream_for(0)  # SL rows; the ADL stream is built on first use
         self.n_tiles = len(tiling.tile_width)
         self.h2d_bytes = int(sum(h2d))
+
+    def stream_for(self, mode: int):
+        """Packed panel stream of the regular sweep: mode 0 (SL rows) or 1
+        (ADL rows) record format (csrc/assemble.cu)."""
+        import torch
+
+        st = self._streams.get(mode)
+        if st is None:
+            rec = _lib.lib().hvb_stream_record_doubles(self.nq, mode)
+            if rec <= 0:
+                raise ValueError(f"no sweep record format for nq={self.nq}")
+            st = torch.empty((self.n_entries, rec), dtype=torch.float64, device=self.device)
+            with torch.cuda.device(self.device):
+                _lib.call("hvb_build_stream", _lib.ptr(self.table), self.nq, _lib.ptr(self.ccr), float(self.cfg.eta),
+                          _lib.ptr(self._ent_tri), _lib.ptr(self._ent_meta), self.n_entries, mode, WINDOW,
+                          _lib.ptr(st), _lib.stream_ptr(self.device))
+            self._streams[mode] = st
+        return st
 
 
 PANEL_GROUP = 32  # csrc/field.cu FCH: panels per shared-memory batch / bound group

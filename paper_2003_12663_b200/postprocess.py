@@ -151,14 +151,19 @@ def _sources(dm, u_dev, key):
 
 
 def _u_device(solution, dm):
+    """Device copy of solution.u plus a key that changes on EVERY upload (the
+    contracted-source cache of ``_sources`` is keyed on it): the host array
+    is compared by content, so an in-place edit of u re-uploads it and
+    invalidates the sources."""
     import torch
 
-    key = (id(solution), solution.u.__array_interface__["data"][0], float(np.sum(solution.u[:3])) if len(solution.u) else 0.0)
     cache = dm.__dict__.setdefault("_u_cache", {})
     hit = cache.get("u")
-    if hit is None or hit[0] != key or not np.array_equal(hit[2], solution.u):
+    if hit is None or hit[2].shape != solution.u.shape or not np.array_equal(hit[2], solution.u):
         u = torch.as_tensor(np.ascontiguousarray(solution.u, dtype=np.float64), device=dm.device)
-        hit = (key, u, np.array(solution.u, copy=True))
+        serial = cache.get("serial", 0) + 1
+        cache["serial"] = serial
+        hit = (("u", serial), u, np.array(solution.u, copy=True))
         cache["u"] = hit
     return hit[1], hit[0]
 

@@ -167,12 +167,29 @@ def test_device_panel_data_matches_host_statement(maker):
     assert np.array_equal(dm.cls.cpu().numpy(), cls)
     assert np.array_equal(dm.ccr.cpu().numpy(), np.column_stack([m.circumcenters, m.circumradii]))
     assert np.array_equal(dm.groups.cpu().numpy(), device.panel_groups(m.circumcenters, m.circumradii, thr))
-    # record tails: slots
-    rec = dm.stream.cpu().numpy()
-    tail = np.ascontiguousarray(rec[:, dm.rec - 2:])
-    slots = tail.view(np.int16).reshape(len(rec), 8)[:, 4:7].astype(np.int64)
+    # record tails (both stream formats): circumcircle bracket and window slots
     loc = dm.tiling.ent_meta[:, 1:4].astype(np.int64)
-    assert np.array_equal(slots, np.where(loc >= 0, loc % dm.window, dm.window))
+    ent = dm.tiling.ent_tri.astype(np.int64)
+    for mode in (0, 1):
+        rec = dm.stream_for(mode).cpu().numpy()
+        assert np.array_equal(rec[:, -8:-5], m.circumcenters[ent])
+        tail = np.ascontiguousarray(rec[:, -2:])
+        slots = tail.view(np.int16).reshape(len(rec), 8)[:, 4:7].astype(np.int64)
+        assert np.array_equal(slots, np.where(loc >= 0, loc % dm.window, dm.window))
+    # SL stream nodes: x'.Y + |x'|^2 Q + P = |x - y|^2 / w^2 (csrc/assemble.cu)
+    nq = dm.nq
+    tab = dm.table.cpu().numpy()[ent]                     # (ne, nq, 6): y, w hat_c
+    y, w = tab[:, :, :3], tab[:, :, 3:].sum(axis=2)
+    rec = dm.stream_for(0).cpu().numpy()
+    pairs = rec[:, :5 * ((nq + 1) & ~1)].reshape(len(rec), -1, 10)
+    Y = np.concatenate([pairs[:, :, None, 0:3], pairs[:, :, None, 6:9]], axis=2).reshape(len(rec), -1, 3)[:, :nq]
+    P = np.stack([pairs[:, :, 3], pairs[:, :, 9]], axis=2).reshape(len(rec), -1)[:, :nq]
+    Q = np.stack([pairs[:, :, 4], pairs[:, :, 5]], axis=2).reshape(len(rec), -1)[:, :nq]
+    x = m.vertices.max(axis=0) + 0.5 * np.ptp(m.vertices, axis=0)   # a far point
+    xc = x[None, :] - m.circumcenters[ent]
+    r2 = np.einsum("ed,eqd->eq", xc, Y) + np.sum(xc * xc, axis=1)[:, None] * Q + P
+    ref = np.sum((x[None, None, :] - y) ** 2, axis=2) / (w * w)
+    assert np.max(np.abs(r2 - ref) / ref) <= 1e-13
     assert dm.h2d_bytes > m.tri_nodes.nbytes
 
 

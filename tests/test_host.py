@@ -44,7 +44,8 @@ def test_binding_signatures_cover_header():
     from paper_2003_12663_b200 import _lib
 
     declared = set(_header_functions()) - {"hvb_last_error", "hvb_version", "hvb_line_state_bytes",
-                                           "hvb_mgs_partial_size", "hvb_ipc_handle_bytes"}
+                                           "hvb_mgs_partial_size", "hvb_ipc_handle_bytes",
+                                           "hvb_stream_record_doubles"}
     assert declared == set(_lib.SIGNATURES)
 
 
