@@ -51,6 +51,25 @@ int hvb_build_stream(const double* table, int nq, const double* ccr, double eta,
                      void* stream);
 int hvb_stream_record_doubles(int nq, int mode);
 
+/* Column tiling of the regular sweep (HOST function, host pointers; no
+ * GPU needed; csrc/tiling.cpp): recursive coordinate bisection of the n
+ * collocation points into tiles of <= max_tile columns swept along their
+ * longest axis, one record per (panel, tile owning one of its corners)
+ * sorted by first owned column, grouped in stages of `group` records with
+ * disjoint owned corners within `band` columns (short stages padded with
+ * dummy records, panel -1).  sizes = (n_tiles, n_records, band, real
+ * records); fetch copies perm (n), tile_col0/width (n_tiles), tile_ptr
+ * (n_tiles + 1), ent_tri (n_records), ent_meta (n_records x 5: mfirst, l0,
+ * l1, l2, flags) and free releases the handle.  Returns 0, 1 (bad
+ * argument) or 2 (band not bounded).
+ * Replaces: nothing in the reference (its rows are independent NumPy
+ * sweeps, assembly.py:173-200); this is the schedule of hvb_assemble_regular. */
+int hvb_tiling_build(const double* points, int n, const int* tri_cols, int nt, int max_tile, int band, int group,
+                     long long* sizes, void** handle);
+int hvb_tiling_fetch(void* handle, int* perm, int* tile_col0, int* tile_width, long long* tile_ptr, int* ent_tri,
+                     int* ent_meta);
+int hvb_tiling_free(void* handle);
+
 /* Per-panel device arrays from the flat circumcircles (cc (nt,3), R (nt)):
  * ccr (nt,4) = cc, R; cls (nt,6) = cc, fl(eta R), fl(eta R)^2 (1 -+ 1e-13);
  * groups (ceil(nt/32), 8) = bounds of aligned 32-panel groups (centre,

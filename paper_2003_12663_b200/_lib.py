@@ -54,6 +54,9 @@ SIGNATURES = {
     "hvb_surface_distance": [_P, _I, _P, _P, _I, _P, _P, _P],
     "hvb_near_coincide": [_P, _LL, _P, _P, _D, _P, _P],
     "hvb_streamer": [_P, _P, _I, _I, _P, _P, _I, _D, _P, _P, _P],
+    "hvb_tiling_build": [_P, _I, _P, _I, _I, _I, _I, _P, _P],
+    "hvb_tiling_fetch": [_P, _P, _P, _P, _P, _P, _P],
+    "hvb_tiling_free": [_P],
     "hvb_bench_dfma": [_P, _I, _I, _P],
     "hvb_bench_read": [_P, _LL, _P, _I, _P],
 }

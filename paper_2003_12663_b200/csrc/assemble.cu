@@ -23,7 +23,10 @@
 //    expansion loses at most ~120 ulp of r2 (~3e-14 relative).
 //  * ADL (MODE 1): per node 6 doubles (y, w hat_0, w hat_1, w hat_2).
 // Both end in an 8-double tail: cc, fl(eta R), bracket lo/hi, panel id,
-// first owned column, window slots of the 3 corners, flags.
+// first owned column, window byte offsets of the 3 corners, flags.  Stages
+// are built by csrc/tiling.cpp: the owned corners of one stage are distinct
+// columns (short stages padded with dummy records), so a stage updates the
+// window with 12 independent read-modify-writes.
 #include <cstdint>
 
 #include "launch.cuh"
@@ -38,13 +41,14 @@ constexpr int WREG = (SLOTS * STRIDE + 1) & ~1;          // doubles per warp win
 constexpr int FLUSH = 16;                                // columns per flush (band <= WIN - FLUSH)
 constexpr int R = 4;                                     // records per stage
 constexpr int WPC = 8;                                   // warps per CTA
-constexpr int S = 3;                                     // ring stages
 
 template <int NQ, int MODE>
 struct Rec {
   static constexpr int NQP = MODE == 0 ? (NQ + 1) & ~1 : NQ;  // SL: node pairs (odd NQ padded)
   static constexpr int DOUBLES = (MODE == 0 ? 5 : 6) * NQP + 8;
   static constexpr int TAIL = DOUBLES - 8;
+  // ring stages: as many as fit two 8-warp CTAs per SM (228 KB) for NQ = 12
+  static constexpr int S = DOUBLES <= 72 ? 4 : 3;
 };
 
 HVB_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -58,7 +62,7 @@ HVB_DEV void mbar_wait(uint64_t* bar, unsigned phase) {
   uint32_t ok = 0;
   while (!ok) {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 100000;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
         : "r"(a), "r"(phase)
         : "memory");
@@ -92,6 +96,7 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
   using namespace sweep;
   using RC = Rec<NQ, MODE>;
   constexpr int REC = RC::DOUBLES;
+  constexpr int S = RC::S;
   extern __shared__ __align__(16) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);         // S mbarriers
   unsigned* released = reinterpret_cast<unsigned*>(smem + S);  // S release counters
@@ -159,6 +164,7 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
     __syncwarp();
   };
 
+  char* const winl = reinterpret_cast<char*>(win) + 8 * lane;  // this lane's row of the window
   for (int p = 0; p < ns; ++p) {
     const int s = p % S;
     sweep::mbar_wait(full + s, (unsigned)(p / S) & 1u);
@@ -168,14 +174,26 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
       flush(base);
       base += FLUSH;
     }
-    // per record: x' = x - cc (IEEE, also the classification's difference)
+    // per record: x' = x - cc (IEEE, also the classification's difference),
+    // the classification, the window byte offsets of its corners
     d3 xc[R];
     double sq[R];
+    bool reg[R], emit[R];
+    int tris[R];
+    unsigned slw[R], sfw[R];  // packed window byte offsets (+ flags)
+    bool any_emit = false;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const double* tl = pr + j * REC + RC::TAIL;
       xc[j] = sub_rn(X0, mk3(tl[0], tl[1], tl[2]));
       sq[j] = fma(xc[j].z, xc[j].z, fma(xc[j].y, xc[j].y, xc[j].x * xc[j].x));
+      reg[j] = sweep::regular(xc[j], sq[j], tl);
+      const int* meta = reinterpret_cast<const int*>(tl + 6);
+      slw[j] = static_cast<unsigned>(meta[2]);
+      sfw[j] = static_cast<unsigned>(meta[3]);
+      tris[j] = meta[0];
+      emit[j] = !reg[j] && ((sfw[j] >> 16) & 1u) && live0;  // from the panel's primary tile only
+      any_emit |= emit[j];
     }
     double acc[R][3];
 #pragma unroll
@@ -222,32 +240,13 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
         }
       }
     }
-    int slots[R][3];
-    bool emit[R];
-    int tris[R];
-    bool any_emit = false;
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const double* tl = pr + j * REC + RC::TAIL;
-      const bool valid = R * p + j < ne;
-      const bool reg = sweep::regular(xc[j], sq[j], tl);
-      if (!reg) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
-      const int* meta = reinterpret_cast<const int*>(tl + 6);
-      const unsigned sl = static_cast<unsigned>(meta[2]), sf = static_cast<unsigned>(meta[3]);
-      slots[j][0] = valid ? (int)(sl & 0xffffu) : WIN;
-      slots[j][1] = valid ? (int)(sl >> 16) : WIN;
-      slots[j][2] = valid ? (int)(sf & 0xffffu) : WIN;
-      const bool prim = valid && (sf >> 16) & 1u;
-      tris[j] = valid ? meta[0] : 0;
-      emit[j] = !reg && prim && live0;
-      any_emit |= emit[j];
-    }
     __syncwarp();
     // this warp is done reading the stage: the last warp to release it
-    // refills it with stage p + S
+    // refills it with stage p + S (every ring value this warp loaded has
+    // been consumed by instructions issued before the release)
     if (lane == 0) {
       unsigned old;
-      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+      asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
                    : "=r"(old)
                    : "r"(sweep::smem_u32(released + s))
                    : "memory");
@@ -256,7 +255,7 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
         if (p + S < ns) issue(p + S);
       }
     }
-    // deferred near pairs (rare): emitted from the panel's primary tile only
+    // deferred near pairs (rare)
     if (__any_sync(0xffffffffu, any_emit)) {
       unsigned msk[R];
       int total = 0;
@@ -284,12 +283,30 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
         off += __popc(msk[j]);
       }
     }
-    // window adds in record order (each lane owns its row: no conflicts)
+    // window update of the whole stage at once: the stage's owned corners are
+    // distinct columns (csrc/tiling.cpp), so the 12 read-modify-writes are
+    // independent; only the never-flushed dump column may collide
+    double wv[R][3];
+    int offs[R][3];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      win[slots[j][0] * STRIDE + lane] += acc[j][0];
-      win[slots[j][1] * STRIDE + lane] += acc[j][1];
-      win[slots[j][2] * STRIDE + lane] += acc[j][2];
+      offs[j][0] = (int)(slw[j] & 0xffffu);
+      offs[j][1] = (int)(slw[j] >> 16);
+      offs[j][2] = (int)(sfw[j] & 0xffffu);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) wv[j][c] = *reinterpret_cast<const double*>(winl + offs[j][c]);
+    }
+    if (__all_sync(0xffffffffu, reg[0] && reg[1] && reg[2] && reg[3])) {  // the common case
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) *reinterpret_cast<double*>(winl + offs[j][c]) = wv[j][c] + acc[j][c];
+    } else {
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          *reinterpret_cast<double*>(winl + offs[j][c]) = reg[j] ? wv[j][c] + acc[j][c] : wv[j][c];
     }
     __syncwarp();
   }
@@ -302,6 +319,7 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
 template <int NQ, int MODE>
 static cudaError_t launch_sweep_nq(const RegularArgs& a, cudaStream_t st) {
   using namespace sweep;
+  constexpr int S = Rec<NQ, MODE>::S;
   const size_t smem = (size_t)(2 * S + S * R * Rec<NQ, MODE>::DOUBLES + WPC * WREG) * sizeof(double);
   static bool init = false;
   if (!init) {
@@ -313,6 +331,8 @@ static cudaError_t launch_sweep_nq(const RegularArgs& a, cudaStream_t st) {
   k_sweep<NQ, MODE><<<grid, 32 * WPC, smem, st>>>(a);
   return cudaGetLastError();
 }
+
+int sweep_window_stride() { return sweep::STRIDE; }
 
 int sweep_record_doubles(int nq, int mode) {
   switch (nq) {

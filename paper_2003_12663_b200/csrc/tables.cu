@@ -93,55 +93,62 @@ __global__ void k_build_stream(const double* __restrict__ table, int nq,
                                const double* __restrict__ ccr,  // (nt,4): cc, R
                                double eta, const int* __restrict__ ent_tri,
                                const int* __restrict__ ent_meta,  // (ne,5): mfirst, slot0, slot1, slot2, flags
-                               int64_t ne, int mode, int rec, int window, double* __restrict__ out) {
+                               int64_t ne, int mode, int rec, int window, int wstride, double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= ne) return;
-  int t = ent_tri[e];
+  const int t = ent_tri[e];  // -1: dummy record padding a stage (no owned corner, never emits)
   double* o = out + e * rec;
-  const double* s = table + (size_t)t * 6 * nq;
-  const double* c = ccr + 4 * (size_t)t;
-  if (mode == 0) {
-    const int nqp = (nq + 1) & ~1;
-    for (int q = 0; q < nqp; ++q) {
-      double Y[3] = {0.0, 0.0, 0.0}, P = 1.0, Q = 0.0;
-      if (q < nq) {
-        const double* y = s + 6 * q;
-        const d3 yc = sub_rn(mk3(y[0], y[1], y[2]), mk3(c[0], c[1], c[2]));
-        const double w = (y[3] + y[4]) + y[5];
-        const double sc = 1.0 / (w * w);
-        Y[0] = -2.0 * sc * yc.x;
-        Y[1] = -2.0 * sc * yc.y;
-        Y[2] = -2.0 * sc * yc.z;
-        P = sc * sumsq_unfused(yc);
-        Q = sc;
-      }
-      double* op = o + 10 * (q >> 1);
-      if ((q & 1) == 0) {
-        op[0] = Y[0]; op[1] = Y[1]; op[2] = Y[2]; op[3] = P; op[4] = Q;
-      } else {
-        op[5] = Q; op[6] = Y[0]; op[7] = Y[1]; op[8] = Y[2]; op[9] = P;
-      }
-    }
+  if (t < 0) {
+    for (int k = 0; k < rec - 2; ++k) o[k] = 0.0;
+    if (mode == 0)
+      for (int q = 0; q < ((nq + 1) & ~1); ++q) o[10 * (q >> 1) + ((q & 1) ? 9 : 3)] = 1.0;  // P = 1: finite
   } else {
-    for (int k = 0; k < 6 * nq; ++k) o[k] = s[k];
+    const double* s = table + (size_t)t * 6 * nq;
+    const double* c = ccr + 4 * (size_t)t;
+    if (mode == 0) {
+      const int nqp = (nq + 1) & ~1;
+      for (int q = 0; q < nqp; ++q) {
+        double Y[3] = {0.0, 0.0, 0.0}, P = 1.0, Q = 0.0;
+        if (q < nq) {
+          const double* y = s + 6 * q;
+          const d3 yc = sub_rn(mk3(y[0], y[1], y[2]), mk3(c[0], c[1], c[2]));
+          const double w = (y[3] + y[4]) + y[5];
+          const double sc = 1.0 / (w * w);
+          Y[0] = -2.0 * sc * yc.x;
+          Y[1] = -2.0 * sc * yc.y;
+          Y[2] = -2.0 * sc * yc.z;
+          P = sc * sumsq_unfused(yc);
+          Q = sc;
+        }
+        double* op = o + 10 * (q >> 1);
+        if ((q & 1) == 0) {
+          op[0] = Y[0]; op[1] = Y[1]; op[2] = Y[2]; op[3] = P; op[4] = Q;
+        } else {
+          op[5] = Q; op[6] = Y[0]; op[7] = Y[1]; op[8] = Y[2]; op[9] = P;
+        }
+      }
+    } else {
+      for (int k = 0; k < 6 * nq; ++k) o[k] = s[k];
+    }
+    const double thr = __dmul_rn(eta, c[3]);
+    const double t2 = thr * thr;
+    double* tail = o + rec - 8;
+    tail[0] = c[0];
+    tail[1] = c[1];
+    tail[2] = c[2];
+    tail[3] = thr;
+    tail[4] = t2 * (1.0 - 1e-13);
+    tail[5] = t2 * (1.0 + 1e-13);
   }
-  double thr = __dmul_rn(eta, c[3]);
-  double t2 = thr * thr;
-  double* tail = o + rec - 8;
-  tail[0] = c[0];
-  tail[1] = c[1];
-  tail[2] = c[2];
-  tail[3] = thr;
-  tail[4] = t2 * (1.0 - 1e-13);
-  tail[5] = t2 * (1.0 + 1e-13);
-  int* m = reinterpret_cast<int*>(tail + 6);
+  int* m = reinterpret_cast<int*>(o + rec - 2);
   const int* em = ent_meta + 5 * e;
-  m[0] = t;
+  m[0] = t < 0 ? 0 : t;
   m[1] = em[0];
   short* l = reinterpret_cast<short*>(m + 2);
-  // window slot of each owned corner (local column mod window); window =
-  // the dump slot for corners owned by another tile
-  for (int c = 0; c < 3; ++c) l[c] = (short)(em[1 + c] >= 0 ? em[1 + c] % window : window);
+  // byte offset of each owned corner's window column (local column mod
+  // window, csrc/assemble.cu WSTRIDE doubles per column); the dump column
+  // (index window) for corners owned by another tile
+  for (int c = 0; c < 3; ++c) l[c] = (short)((em[1 + c] >= 0 ? em[1 + c] % window : window) * wstride * 8);
   l[3] = (short)em[4];
 }
 
@@ -234,7 +241,7 @@ cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, 
   const int rec = sweep_record_doubles(nq, mode);
   if (rec < 0) return cudaErrorInvalidValue;
   k_build_stream<<<(unsigned)((ne + 127) / 128), 128, 0, st>>>(table, nq, ccr, eta, ent_tri, ent_meta, ne, mode, rec,
-                                                              window, out);
+                                                              window, sweep_window_stride(), out);
   return cudaGetLastError();
 }
 

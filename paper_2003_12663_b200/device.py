@@ -56,124 +56,45 @@ class ColumnTiling:
     redundancy: float
 
 
-def _rcb(points: np.ndarray, idx: np.ndarray, max_tile: int, out: list):
-    """Recursive coordinate bisection (median split on the longest axis)."""
-    stack = [idx]
-    while stack:
-        cur = stack.pop()
-        if len(cur) <= max_tile:
-            out.append(cur)
-            continue
-        p = points[cur]
-        ax = int(np.argmax(p.max(axis=0) - p.min(axis=0)))
-        order = np.argsort(p[:, ax], kind="stable")
-        h = len(cur) // 2
-        # push the second half first so tiles come out in sweep order
-        stack.append(cur[order[h:]])
-        stack.append(cur[order[:h]])
+def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = MAX_TILE, band_max: int = WINDOW - FLUSH,
+                  group: int = GROUP) -> ColumnTiling:
+    """Column tiles + grouped (tile, panel) records, built natively
+    (csrc/tiling.cpp, host C++): recursive coordinate bisection into tiles
+    of <= max_tile columns swept along their longest axis; records sorted by
+    first owned column and grouped in stages of ``group`` whose owned corners
+    are disjoint and lie within ``band_max`` columns of the stage's first
+    record (short stages padded with dummy records, panel -1); tiles whose
+    records span more than ``band_max`` columns are halved across their sweep
+    direction.  ``redundancy`` = real records per panel."""
+    import ctypes
 
-
-def _sweep(points: np.ndarray, tile: np.ndarray) -> np.ndarray:
-    p = points[tile]
-    ax = int(np.argmax(p.max(axis=0) - p.min(axis=0)))
-    return tile[np.argsort(p[:, ax], kind="stable")]
-
-
-def _entries(tri_cols: np.ndarray, tile_of: np.ndarray, local: np.ndarray):
-    nt = len(tri_cols)
-    ct = tile_of[tri_cols]  # (nt, 3) tile of each corner
-    cl = local[tri_cols]
-    tri = np.repeat(np.arange(nt), 3)
-    tl = ct.ravel()
-    # unique (panel, tile) pairs
-    key = tri.astype(np.int64) * (int(tile_of.max()) + 1) + tl
-    key = np.unique(key)
-    e_tri = key // (int(tile_of.max()) + 1)
-    e_tile = key % (int(tile_of.max()) + 1)
-    owned = ct[e_tri] == e_tile[:, None]  # (ne, 3)
-    loc = np.where(owned, cl[e_tri], -1)
-    big = np.iinfo(np.int64).max
-    mfirst = np.where(owned, loc, big).min(axis=1)
-    mlast = np.where(owned, loc, -1).max(axis=1)
-    primary = (ct[e_tri, 0] == e_tile).astype(np.int64)
-    return e_tri, e_tile, loc, mfirst, mlast, primary
-
-
-def _split_across(points: np.ndarray, tile: np.ndarray):
-    """Halve a tile across its sweep direction (median split on the
-    second-longest axis): the sweep front halves, the tile stays a strip."""
-    p = points[tile]
-    ext = p.max(axis=0) - p.min(axis=0)
-    ax = int(np.argsort(ext)[-2])
-    order = np.argsort(p[:, ax], kind="stable")
-    h = len(tile) // 2
-    return [tile[order[:h]], tile[order[h:]]]
-
-
-def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = 2048,
-                  band_max: int = WINDOW - FLUSH, group: int = GROUP, strips: bool = False) -> ColumnTiling:
-    """Column tiles + sorted (tile, panel) entries.  The band is measured
-    over groups of ``group`` consecutive records of each tile (starting at
-    the tile's first record), as the grouped assembly kernel keeps a whole
-    group in its window at once.  ``strips``: tiles of up to ``max_tile``
-    columns that violate the band are split ACROSS their sweep axis (long
-    strips, fewer boundary panels) instead of recursively bisected."""
-    n = len(points)
-    tri_cols = np.asarray(tri_cols, dtype=np.int64)
-    tiles: list = []
-    _rcb(points, np.arange(n), max_tile, tiles)
-    for _ in range(40):
-        tiles = [_sweep(points, t) for t in tiles]
-        tile_of = np.empty(n, dtype=np.int64)
-        local = np.empty(n, dtype=np.int64)
-        for k, t in enumerate(tiles):
-            tile_of[t] = k
-            local[t] = np.arange(len(t))
-        e_tri, e_tile, loc, mfirst, mlast, primary = _entries(tri_cols, tile_of, local)
-        order = np.lexsort((e_tri, mfirst, e_tile))
-        e_tri, e_tile, loc, mfirst, mlast, primary = (x[order] for x in (e_tri, e_tile, loc, mfirst, mlast,
-                                                                          primary))
-        counts = np.bincount(e_tile, minlength=len(tiles))
-        tile_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-        band_e = mlast - mfirst
-        if group > 1 and len(e_tri):
-            pos = np.arange(len(e_tri)) - tile_ptr[e_tile]
-            gid = e_tile * (int(counts.max()) + group) + pos // group  # group key
-            first = np.nonzero(pos % group == 0)[0]
-            gmax = np.full(len(e_tri), -1, dtype=np.int64)
-            np.maximum.at(gmax, np.searchsorted(gid[first], gid), mlast)
-            band_e = np.zeros_like(band_e)
-            band_e[first] = gmax[: len(first)] - mfirst[first]
-        per_tile = np.zeros(len(tiles), dtype=np.int64)
-        np.maximum.at(per_tile, e_tile, band_e)
-        bad = np.nonzero(per_tile > band_max)[0]
-        if len(bad) == 0:
-            break
-        bad_set = set(bad.tolist())
-        nxt: list = []
-        for k, t in enumerate(tiles):
-            if k in bad_set and len(t) > 1:
-                if strips:
-                    nxt.extend(_split_across(points, t))
-                else:
-                    _rcb(points, t, max(1, len(t) // 2), nxt)
-            else:
-                nxt.append(t)
-        tiles = nxt
-    else:  # pragma: no cover - pathological mesh
-        raise RuntimeError("column tiling: could not bound the panel band")
-    perm = np.concatenate(tiles).astype(np.int64)
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    tc = np.ascontiguousarray(tri_cols, dtype=np.int32)
+    n, nt = len(pts), len(tc)
+    h = _lib.lib()
+    sizes = np.zeros(4, dtype=np.int64)
+    handle = ctypes.c_void_p()
+    rc = h.hvb_tiling_build(pts.ctypes.data_as(ctypes.c_void_p), n, tc.ctypes.data_as(ctypes.c_void_p), nt,
+                            int(max_tile), int(band_max), int(group), sizes.ctypes.data_as(ctypes.c_void_p),
+                            ctypes.byref(handle))
+    if rc != 0:
+        raise RuntimeError("column tiling failed" + (": could not bound the panel band" if rc == 2 else ""))
+    n_tiles, ne, band, real = (int(x) for x in sizes)
+    perm = np.empty(n, dtype=np.int32)
+    col0 = np.empty(n_tiles, dtype=np.int32)
+    width = np.empty(n_tiles, dtype=np.int32)
+    ptr = np.empty(n_tiles + 1, dtype=np.int64)
+    ent_tri = np.empty(ne, dtype=np.int32)
+    ent_meta = np.empty((ne, 5), dtype=np.int32)
+    try:
+        h.hvb_tiling_fetch(handle, *(a.ctypes.data_as(ctypes.c_void_p) for a in (perm, col0, width, ptr, ent_tri,
+                                                                                 ent_meta)))
+    finally:
+        h.hvb_tiling_free(handle)
     inv = np.empty(n, dtype=np.int64)
     inv[perm] = np.arange(n)
-    widths = np.array([len(t) for t in tiles], dtype=np.int64)
-    col0 = np.concatenate([[0], np.cumsum(widths)[:-1]])
-    meta = np.column_stack([mfirst, loc, primary]).astype(np.int32)
-    return ColumnTiling(
-        perm=perm, inv=inv, tile_col0=col0.astype(np.int32), tile_width=widths.astype(np.int32),
-        tile_ptr=tile_ptr, ent_tri=e_tri.astype(np.int32), ent_meta=meta,
-        band=int(per_tile.max()) if len(per_tile) else 0,
-        redundancy=float(len(e_tri)) / max(1, len(tri_cols)),
-    )
+    return ColumnTiling(perm=perm.astype(np.int64), inv=inv, tile_col0=col0, tile_width=width, tile_ptr=ptr,
+                        ent_tri=ent_tri, ent_meta=ent_meta, band=band, redundancy=real / max(1, nt))
 
 
 def _rule4(rule) -> np.ndarray:
@@ -239,7 +160,7 @@ class DeviceMesh:
 
         # column tiling + panel streams
         self.window = WINDOW
-        tiling = mesh_tiling(mesh, max_tile, WINDOW, True, GROUP, FLUSH)
+        tiling = mesh_tiling(mesh, max_tile)
         self.tiling = tiling
         self.perm = up(tiling.perm, **i32)
         self.col_dev = up(tiling.inv, **i32)
@@ -301,15 +222,13 @@ def panel_groups(cc: np.ndarray, radii: np.ndarray, thr: np.ndarray) -> np.ndarr
     return out
 
 
-def mesh_tiling(mesh, max_tile: int = 2048, window: int = 96, strips: bool = False, group: int = 2,
-                flush: int = 32) -> ColumnTiling:
-    """Host column tiling of a mesh (a mesh-derived array, cached on it)."""
-    key = ("tiling", max_tile, window, strips, group, flush)
+def mesh_tiling(mesh, max_tile: int = MAX_TILE) -> ColumnTiling:
+    """Column tiling of a mesh (a mesh-derived array, cached on it)."""
+    key = ("tiling", max_tile, WINDOW, FLUSH, GROUP)
     cache = mesh._device_cache
     t = cache.get(key)
     if t is None:
-        t = column_tiling(mesh.colloc_points, mesh.tri_corner_cols, max_tile=max_tile, band_max=window - flush,
-                          group=group, strips=strips)
+        t = column_tiling(mesh.colloc_points, mesh.tri_corner_cols, max_tile=max_tile)
         cache[key] = t
     return t
 

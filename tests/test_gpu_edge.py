@@ -169,18 +169,21 @@ def test_device_panel_data_matches_host_statement(maker):
     assert np.array_equal(dm.groups.cpu().numpy(), device.panel_groups(m.circumcenters, m.circumradii, thr))
     # record tails (both stream formats): circumcircle bracket and window slots
     loc = dm.tiling.ent_meta[:, 1:4].astype(np.int64)
-    ent = dm.tiling.ent_tri.astype(np.int64)
+    real = dm.tiling.ent_tri >= 0                     # dummy records (-1) pad short stages
+    ent = dm.tiling.ent_tri[real].astype(np.int64)
     for mode in (0, 1):
         rec = dm.stream_for(mode).cpu().numpy()
-        assert np.array_equal(rec[:, -8:-5], m.circumcenters[ent])
+        assert np.array_equal(rec[real][:, -8:-5], m.circumcenters[ent])
         tail = np.ascontiguousarray(rec[:, -2:])
-        slots = tail.view(np.int16).reshape(len(rec), 8)[:, 4:7].astype(np.int64)
-        assert np.array_equal(slots, np.where(loc >= 0, loc % dm.window, dm.window))
+        offs = tail.view(np.uint16).reshape(len(rec), 8)[:, 4:7].astype(np.int64)
+        assert np.array_equal(offs, np.where(loc >= 0, loc % dm.window, dm.window) * 33 * 8)  # 33: window stride
+        flags = tail.view(np.uint16).reshape(len(rec), 8)[:, 7]
+        assert not np.any(flags[~real])
     # SL stream nodes: x'.Y + |x'|^2 Q + P = |x - y|^2 / w^2 (csrc/assemble.cu)
     nq = dm.nq
     tab = dm.table.cpu().numpy()[ent]                     # (ne, nq, 6): y, w hat_c
     y, w = tab[:, :, :3], tab[:, :, 3:].sum(axis=2)
-    rec = dm.stream_for(0).cpu().numpy()
+    rec = dm.stream_for(0).cpu().numpy()[real]
     pairs = rec[:, :5 * ((nq + 1) & ~1)].reshape(len(rec), -1, 10)
     Y = np.concatenate([pairs[:, :, None, 0:3], pairs[:, :, None, 6:9]], axis=2).reshape(len(rec), -1, 3)[:, :nq]
     P = np.stack([pairs[:, :, 3], pairs[:, :, 9]], axis=2).reshape(len(rec), -1)[:, :nq]

@@ -432,3 +432,49 @@ def test_import_alias_drop_in():
         for k in [k for k in sys.modules if k == "hvbem" or k.startswith("hvbem.")]:
             del sys.modules[k]
         sys.modules.update(saved)
+
+
+@pytest.mark.parametrize("scale", [0.12, 0.4])
+def test_column_tiling_invariants(scale):
+    """csrc/tiling.cpp (host C++, no GPU): the device column order is a
+    permutation; every (panel, tile owning one of its corners) record exists
+    once with its owned corners; stages of 4 records have pairwise disjoint
+    owned columns within the 32-column band of their first record, whose
+    first owned column is the stage minimum; stage starts never decrease
+    within a tile; dummies (-1) only pad stages."""
+    from paper_2003_12663_b200 import device, fixtures
+
+    m = fixtures.rod_plane_mesh(scale)
+    T = device.column_tiling(m.colloc_points, m.tri_corner_cols, max_tile=2048)
+    n = m.n_collocation
+    assert np.array_equal(np.sort(T.perm), np.arange(n))
+    assert T.tile_col0[0] == 0 and T.tile_col0[-1] + T.tile_width[-1] == n
+    tile_of = np.repeat(np.arange(len(T.tile_width)), T.tile_width)[T.inv]
+    local = T.inv - T.tile_col0[tile_of]
+    seen = set()
+    for k in range(len(T.tile_width)):
+        a, b = int(T.tile_ptr[k]), int(T.tile_ptr[k + 1])
+        assert (b - a) % 4 == 0
+        prev = -1
+        for s0 in range(a, b, 4):
+            st = range(s0, s0 + 4)
+            cols = [c for e in st for c in T.ent_meta[e, 1:4] if c >= 0]
+            assert len(cols) == len(set(cols))                       # disjoint owned corners
+            start = T.ent_meta[s0, 0]
+            assert T.ent_tri[s0] >= 0 and start >= prev
+            prev = start
+            for e in st:
+                t = int(T.ent_tri[e])
+                if t < 0:
+                    assert np.all(T.ent_meta[e, 1:4] == -1) and T.ent_meta[e, 4] == 0
+                    continue
+                own = [c for c in T.ent_meta[e, 1:4] if c >= 0]
+                assert min(own) == T.ent_meta[e, 0] >= start and max(own) <= start + 32
+                corners = m.tri_corner_cols[t]
+                exp = [int(local[c]) if tile_of[c] == k else -1 for c in corners]
+                assert list(T.ent_meta[e, 1:4]) == exp
+                assert T.ent_meta[e, 4] == int(tile_of[corners[0]] == k)
+                assert (t, k) not in seen
+                seen.add((t, k))
+    want = {(t, int(tile_of[c])) for t in range(m.n_triangles) for c in m.tri_corner_cols[t]}
+    assert seen == want
