@@ -92,7 +92,7 @@ int hvb_panel_data(const double* circumcenters, const double* radii, int nt, dou
 int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_col0,
                          const int* tile_width, int n_tiles, int nq, const double* hats, int row_begin, int n_rows,
                          const double* rowdata, const int* row_col, const double* row_scale,
-                         const long long* row_out, double* A, const int* tri_cols, int mode,
+                         const long long* row_out, double* A, long long part_ld, const int* tri_cols, int mode,
                          int* near_list, unsigned long long* near_count, long long near_cap, void* stream);
 
 /* K4 (+K6 diagonal) -- singular corner pairs with the split-corner Duffy
@@ -102,7 +102,8 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
 int hvb_assemble_singular(const double* nodes6, const int* tri_cols, const int* col_dev, const int* vc_ptr,
                           const int* vc_tri, const int* vc_corner, const double* rule, int n_rule, int n_rows,
                           const double* rowdata, const int* row_kind, const int* row_col, const double* row_scale,
-                          const double* row_diag, const long long* row_out, double* A, void* stream);
+                          const double* row_diag, const long long* row_out, double* A, int rows_per_warp,
+                          void* stream);
 
 /* K6 -- floating-potential columns n..n+n_fl-1 of collocation rows (-1 in
  * the row's own floating column).  Replaces: _row_equation 425-426 */
@@ -119,6 +120,18 @@ int hvb_near_pairs(const int* pairs, long long n_pairs, const double* points, co
                    void* stream);
 
 /* add sorted near-pair contributions to matrix rows (deterministic order) */
+/* K7 -- charge / neutrality row (charge-reduce mode).  hvb_assemble_regular
+ * with part_ld > 0 (ADL rows, row_begin % 32 == 0) writes, per 32-row tile
+ * t, part[t][c] = sum over the tile's rows of row_scale * (regular entry c)
+ * instead of the rows; hvb_near_apply_rows (segments per tile, row_out[r] =
+ * t * part_ld) and hvb_assemble_singular (rows_per_warp = 32) then add the
+ * near, singular and diagonal (row_diag) terms into the same partial rows
+ * in a fixed order, and hvb_charge_reduce sums them: out[c] (+)= sum_t
+ * part[t][c] (accumulate = 1 adds to out: chunk partials in chunk order).
+ * Replaces: charge_row  assembly.py:540-569, neutrality rows 441-468 */
+int hvb_charge_reduce(const double* part, int n_parts, long long part_ld, int n, double* out, int accumulate,
+                      void* stream);
+
 int hvb_near_apply_rows(const int* seg_ptr, int n_seg, const int* pairs, const double* contrib,
                         const int* tri_cols, const int* col_dev, const double* row_scale, const long long* row_out,
                         double* A, void* stream);

@@ -359,18 +359,20 @@ def _span(label, e0):
         PROFILE.append((label, e0, _mark()))
 
 
-def _run_rows(dm, plan: RowPlan, A, counts: dict):
-    """Regular + near + singular passes for one row plan writing into A."""
+def _run_rows(dm, plan: RowPlan, A, counts: dict, part_ld: int = 0):
+    """Regular + near + singular passes for one row plan writing into A.
+    part_ld > 0 (charge-reduce mode, ADL rows only): A holds one partial row
+    per 32-row tile and plan.out[r] must be (r // 32) * part_ld."""
     import torch
 
     dev = dm.device
     if plan.m == 0:
         return
     with torch.cuda.device(dev):
-        _run_rows_on(dm, plan, A, counts)
+        _run_rows_on(dm, plan, A, counts, part_ld)
 
 
-def _run_rows_on(dm, plan: RowPlan, A, counts: dict):
+def _run_rows_on(dm, plan: RowPlan, A, counts: dict, part_ld: int = 0):
     import torch
 
     dev = dm.device
@@ -387,7 +389,7 @@ def _run_rows_on(dm, plan: RowPlan, A, counts: dict):
                     "hvb_assemble_regular", _lib.ptr(dm.stream_for(mode)), _lib.ptr(dm.tile_ptr),
                     _lib.ptr(dm.tile_col0), _lib.ptr(dm.tile_width), dm.n_tiles, dm.nq, hats, lo, hi - lo,
                     _lib.ptr(plan.rowdata), _lib.ptr(plan.col), _lib.ptr(plan.scale), _lib.ptr(plan.out),
-                    _lib.ptr(A), _lib.ptr(dm.tri_cols), mode, _lib.ptr(near), _lib.ptr(cnt), cap, s)
+                    _lib.ptr(A), part_ld, _lib.ptr(dm.tri_cols), mode, _lib.ptr(near), _lib.ptr(cnt), cap, s)
         n_near = int(cnt.item())
         if n_near <= cap:
             break
@@ -405,7 +407,8 @@ def _run_rows_on(dm, plan: RowPlan, A, counts: dict):
                   _lib.ptr(dm.nodes6), _lib.ptr(dm.radii), _lib.ptr(dm.rule_near), len(dm.rule_near),
                   _lib.ptr(dm.rule_graded), len(dm.rule_graded), int(dm.cfg.bisect_depth),
                   float(dm.cfg.bisect_trigger), _lib.ptr(contrib), s)
-        seg = _segments(pairs[:, 0])
+        # one sequential segment per row (per 32-row tile in charge-reduce mode)
+        seg = _segments(pairs[:, 0] // 32 if part_ld else pairs[:, 0])
         _lib.call("hvb_near_apply_rows", _lib.ptr(seg), len(seg) - 1, _lib.ptr(pairs), _lib.ptr(contrib),
                   _lib.ptr(dm.tri_cols), _lib.ptr(dm.col_dev), _lib.ptr(plan.scale), _lib.ptr(plan.out),
                   _lib.ptr(A), s)
@@ -414,7 +417,7 @@ def _run_rows_on(dm, plan: RowPlan, A, counts: dict):
     _lib.call("hvb_assemble_singular", _lib.ptr(dm.nodes6), _lib.ptr(dm.tri_cols), _lib.ptr(dm.col_dev),
               _lib.ptr(dm.vc_ptr), _lib.ptr(dm.vc_tri), _lib.ptr(dm.vc_corner), _lib.ptr(dm.rule_duffy),
               dm.n_duffy, plan.m, _lib.ptr(plan.rowdata), _lib.ptr(plan.kind), _lib.ptr(plan.col),
-              _lib.ptr(plan.scale), _lib.ptr(plan.diag), _lib.ptr(plan.out), _lib.ptr(A), s)
+              _lib.ptr(plan.scale), _lib.ptr(plan.diag), _lib.ptr(plan.out), _lib.ptr(A), 32 if part_ld else 1, s)
     _span("singular", e_sing)
 
 
@@ -466,33 +469,51 @@ def _neutrality_scales(mesh, k: int):
 NEUTRALITY_CHUNK = 4096  # members per partial sum of a neutrality / charge row
 
 
-def adl_chunk_sum(mesh, dm, mem, adl_scale, id_scale):
-    """Partial sum_i w_i adl ADL_i + w_i id e_i over one chunk of members, in
-    DEVICE column order (the unit the neutrality rows are split into)."""
+def _charge_chunk(mesh, dm, mem, adl_scale, id_scale, out, accumulate: bool):
+    """out (+)= sum_i w_i adl ADL_i + w_i id e_i over one chunk of members, in
+    DEVICE column order, fused (csrc/assemble.cu charge-reduce mode): the
+    sweep writes one partial row per 32 members, the near / singular /
+    diagonal terms are added into the same partial rows in a fixed order and
+    hvb_charge_reduce sums the partial rows in order -- no (members, N)
+    scratch."""
     import torch
 
     n = mesh.n_collocation
     lda = -(-n // LDA_ALIGN) * LDA_ALIGN
     mem = np.asarray(mem, dtype=np.int64)
+    m = len(mem)
+    tiles = -(-m // 32)
     w = mesh.lumped_weights[mem]
-    scratch = torch.empty((len(mem), lda), dtype=torch.float64, device=dm.device)
-    plan = _plan(dm.device, mesh.colloc_points[mem], mesh.colloc_normals[mem], np.ones(len(mem), np.int64),
-                 mem, w * adl_scale, w * id_scale, np.arange(len(mem)) * lda)
-    _run_rows(dm, plan, scratch, {"near": 0})
-    return scratch[:, :n].sum(dim=0)
+    part = torch.empty((tiles, lda), dtype=torch.float64, device=dm.device)
+    plan = _plan(dm.device, mesh.colloc_points[mem], mesh.colloc_normals[mem], np.ones(m, np.int64), mem,
+                 w * adl_scale, w * id_scale, (np.arange(m) // 32) * lda)
+    _run_rows(dm, plan, part, {"near": 0}, part_ld=lda)
+    with torch.cuda.device(dm.device):
+        _lib.call("hvb_charge_reduce", _lib.ptr(part), tiles, lda, n, _lib.ptr(out), int(accumulate),
+                  _lib.stream_ptr(dm.device))
+    return out
+
+
+def adl_chunk_sum(mesh, dm, mem, adl_scale, id_scale):
+    """Partial sum_i w_i adl ADL_i + w_i id e_i over one chunk of members, in
+    DEVICE column order (the unit the neutrality rows are split into)."""
+    import torch
+
+    out = torch.empty(mesh.n_collocation, dtype=torch.float64, device=dm.device)
+    return _charge_chunk(mesh, dm, mem, adl_scale, id_scale, out, accumulate=False)
 
 
 def _weighted_adl_sum(mesh, dm, members, adl_scale, id_scale, chunk: int | None = None):
     """sum_i w_i adl ADL_i + w_i id e_i over `members`, in DEVICE column
-    order: chunk partials (adl_chunk_sum) added in chunk order -- the same
-    order parallel.assemble_distributed uses when the chunks are spread over
+    order: chunk partials added in chunk order -- the same order
+    parallel.assemble_distributed uses when the chunks are spread over
     ranks, so the row is bitwise independent of the GPU count."""
     import torch
 
     chunk = chunk or NEUTRALITY_CHUNK
     acc = torch.zeros(mesh.n_collocation, dtype=torch.float64, device=dm.device)
     for c0 in range(0, len(members), chunk):
-        acc += adl_chunk_sum(mesh, dm, members[c0:c0 + chunk], adl_scale, id_scale)
+        _charge_chunk(mesh, dm, members[c0:c0 + chunk], adl_scale, id_scale, acc, accumulate=True)
     return acc
 
 

@@ -91,7 +91,11 @@ HVB_DEV bool regular(d3 d, double sq, const double* tail) {
 }
 }  // namespace sweep
 
-template <int NQ, int MODE>
+// RED (charge-reduce mode, MODE 1 only): instead of one row per lane, the
+// flush writes the scaled sum over the warp's 32 rows of every column into
+// the tile's partial row a.A + tile * a.part_ld (csrc/tables.cu
+// k_charge_reduce then sums the partial rows in order).
+template <int NQ, int MODE, bool RED = false>
 __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
   using namespace sweep;
   using RC = Rec<NQ, MODE>;
@@ -139,8 +143,9 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
   const d3 X0 = mk3(rd0[0], rd0[1], rd0[2]);
   const d3 N0 = mk3(rd0[3], rd0[4], rd0[5]);
   const int own0 = a.row_col[lr0];
-  const int64_t fout = live0 ? a.row_out[lr0] : -1;
-  const double fscale = a.row_scale[lr0] * (MODE == 0 ? 0.5 : 1.0);  // SL sums hold 2w/r (exact halving)
+  const int64_t fout = live0 ? (RED ? 0 : a.row_out[lr0]) : -1;
+  const double fscale = live0 ? a.row_scale[lr0] * (MODE == 0 ? 0.5 : 1.0) : 0.0;  // SL sums hold 2w/r
+  double* const part = RED ? a.A + (int64_t)((a.row_begin + base_row) / ROWS) * a.part_ld : nullptr;
 
   for (int k = lane; k < SLOTS * STRIDE; k += 32) win[k] = 0.0;
 
@@ -153,13 +158,25 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
     double* wcol = win + (c % WIN) * STRIDE;
     const bool in = c < width;
     const int rh = (lane >> 4) * 16;
+    if (RED) {
+      double sum = 0.0;  // rows rh .. rh+15 in order, then the two halves
 #pragma unroll 8
-    for (int j = 0; j < 16; ++j) {
-      const int row = rh + j;
-      const int64_t off = __shfl_sync(0xffffffffu, fout, row);
-      const double sc = __shfl_sync(0xffffffffu, fscale, row);
-      if (off >= 0 && in) a.A[off + col0 + c] = wcol[row] * sc;
-      wcol[row] = 0.0;
+      for (int j = 0; j < 16; ++j) {
+        const int row = rh + j;
+        sum = fma(wcol[row], __shfl_sync(0xffffffffu, fscale, row), sum);
+        wcol[row] = 0.0;
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 16);
+      if (lane < 16 && in) part[col0 + c] = sum;
+    } else {
+#pragma unroll 8
+      for (int j = 0; j < 16; ++j) {
+        const int row = rh + j;
+        const int64_t off = __shfl_sync(0xffffffffu, fout, row);
+        const double sc = __shfl_sync(0xffffffffu, fscale, row);
+        if (off >= 0 && in) a.A[off + col0 + c] = wcol[row] * sc;
+        wcol[row] = 0.0;
+      }
     }
     __syncwarp();
   };
@@ -316,19 +333,20 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
   }
 }
 
-template <int NQ, int MODE>
+template <int NQ, int MODE, bool RED = false>
 static cudaError_t launch_sweep_nq(const RegularArgs& a, cudaStream_t st) {
   using namespace sweep;
   constexpr int S = Rec<NQ, MODE>::S;
   const size_t smem = (size_t)(2 * S + S * R * Rec<NQ, MODE>::DOUBLES + WPC * WREG) * sizeof(double);
   static bool init = false;
   if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(k_sweep<NQ, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_sweep<NQ, MODE, RED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     init = true;
   }
   dim3 grid((a.n_rows + ROWS * WPC - 1) / (ROWS * WPC), a.n_tiles);
-  k_sweep<NQ, MODE><<<grid, 32 * WPC, smem, st>>>(a);
+  k_sweep<NQ, MODE, RED><<<grid, 32 * WPC, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -349,6 +367,7 @@ cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, cudaStream_t 
   if (a.n_rows <= 0 || a.n_tiles <= 0) return cudaSuccess;
   auto go = [&](auto nq_tag) -> cudaError_t {
     constexpr int Q = decltype(nq_tag)::value;
+    if (a.part_ld > 0) return launch_sweep_nq<Q, 1, true>(a, st);
     return mode == 0 ? launch_sweep_nq<Q, 0>(a, st) : launch_sweep_nq<Q, 1>(a, st);
   };
   switch (nq) {

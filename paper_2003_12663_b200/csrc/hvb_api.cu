@@ -63,9 +63,11 @@ int hvb_stream_record_doubles(int nq, int mode) { return hvb::sweep_record_doubl
 int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_col0,
                          const int* tile_width, int n_tiles, int nq, const double* hats, int row_begin, int n_rows,
                          const double* rowdata, const int* row_col, const double* row_scale,
-                         const long long* row_out, double* A, const int* tri_cols, int mode,
+                         const long long* row_out, double* A, long long part_ld, const int* tri_cols, int mode,
                          int* near_list, unsigned long long* near_count, long long near_cap, void* stream) {
   if (n_rows <= 0 || n_tiles <= 0) return HVB_OK;
+  if (part_ld < 0 || (part_ld > 0 && (mode != 1 || row_begin % 32 != 0)))
+    return fail(HVB_EARG, "hvb_assemble_regular: charge-reduce mode needs ADL rows starting at a 32-row boundary");
   if (mode != 0 && mode != 1) return fail(HVB_EARG, "hvb_assemble_regular: mode must be 0 (SL) or 1 (ADL)");
   if (hvb::sweep_record_doubles(nq, mode) < 0) return fail(HVB_EARG, "hvb_assemble_regular: nq must be 3, 6, 12 or 16");
   if (mode == 0 && !hats) return fail(HVB_EARG, "hvb_assemble_regular: the SL sweep needs the hat table");
@@ -87,6 +89,7 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
   a.near_list = near_list;
   a.near_count = near_count;
   a.near_cap = near_cap;
+  a.part_ld = part_ld;
   if (hats)
     for (int q = 0; q < nq; ++q)
       for (int c = 0; c < 3; ++c) a.hats[q][c] = hats[3 * q + c];
@@ -96,8 +99,11 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
 int hvb_assemble_singular(const double* nodes6, const int* tri_cols, const int* col_dev, const int* vc_ptr,
                           const int* vc_tri, const int* vc_corner, const double* rule, int n_rule, int n_rows,
                           const double* rowdata, const int* row_kind, const int* row_col, const double* row_scale,
-                          const double* row_diag, const long long* row_out, double* A, void* stream) {
+                          const double* row_diag, const long long* row_out, double* A, int rows_per_warp,
+                          void* stream) {
+  if (rows_per_warp < 1) return fail(HVB_EARG, "hvb_assemble_singular: rows_per_warp must be >= 1");
   hvb::SingularArgs a;
+  a.rows_per_warp = rows_per_warp;
   a.nodes6 = nodes6;
   a.tri_cols = tri_cols;
   a.col_dev = col_dev;
@@ -116,6 +122,13 @@ int hvb_assemble_singular(const double* nodes6, const int* tri_cols, const int* 
   a.row_out = (const int64_t*)row_out;
   a.A = A;
   return check(hvb::launch_singular(a, (cudaStream_t)stream), "hvb_assemble_singular");
+}
+
+int hvb_charge_reduce(const double* part, int n_parts, long long part_ld, int n, double* out, int accumulate,
+                      void* stream) {
+  if (n_parts < 0 || n < 0 || part_ld < n) return fail(HVB_EARG, "hvb_charge_reduce: bad n_parts / n / part_ld");
+  return check(hvb::launch_charge_reduce(part, n_parts, part_ld, n, out, accumulate, (cudaStream_t)stream),
+               "hvb_charge_reduce");
 }
 
 int hvb_fill_float_cols(double* A, const long long* row_out, const int* row_float, int n_rows, int n, int n_fl,

@@ -25,6 +25,8 @@ struct RegularArgs {
   unsigned long long* near_count;
   long long near_cap;
   double hats[16][3];       // hat_c(q) of the regular rule (SL stream; zero past nq)
+  int64_t part_ld;          // > 0: charge-reduce mode (ADL rows only): A holds one partial
+                            // row per 32-row tile, sum over the tile's rows of row_scale * entry
 };
 
 struct SingularArgs {
@@ -45,6 +47,7 @@ struct SingularArgs {
   const double* row_diag;  // added to A[row, own col] after scaling
   const int64_t* row_out;
   double* A;
+  int rows_per_warp;       // 1; 32 in charge-reduce mode (a tile's rows share one partial row)
 };
 
 struct NearArgs {
@@ -93,6 +96,8 @@ cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, 
 cudaError_t launch_panel_data(const double* cc, const double* radii, int nt, double eta, double* ccr, double* cls,
                               double* groups, cudaStream_t st);
 cudaError_t launch_singular(const SingularArgs& a, cudaStream_t st);
+cudaError_t launch_charge_reduce(const double* part, int n_parts, int64_t part_ld, int n, double* out, int accumulate,
+                                 cudaStream_t st);
 cudaError_t launch_fill_float_cols(double* A, const int64_t* row_out, const int* row_float, int n_rows, int n,
                                    int n_fl, cudaStream_t st);
 cudaError_t launch_near_pairs(const NearArgs& a, cudaStream_t st);

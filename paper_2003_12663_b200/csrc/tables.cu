@@ -160,46 +160,62 @@ __global__ void k_build_stream(const double* __restrict__ table, int nq,
 
 __global__ void k_assemble_singular(SingularArgs a) {
   const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (w >= a.n_rows) return;
-  const double* rd = a.rowdata + 6 * (size_t)w;
-  const d3 X = mk3(rd[0], rd[1], rd[2]);
-  const double nx = rd[3], ny = rd[4], nz = rd[5];
-  const bool adl = a.row_kind[w] == 1;
-  const int own = a.row_col[w];
-  const double sc = a.row_scale[w];
-  double* Arow = a.A + a.row_out[w];
-  if (own < 0) return;
-  for (int s = a.vc_ptr[own]; s < a.vc_ptr[own + 1]; ++s) {
-    const int t = a.vc_tri[s], c = a.vc_corner[s];
-    const double* Xn = a.nodes6 + 18 * (size_t)t;
-    const double* R = a.rule + (size_t)c * a.nm * 4;
-    double s0 = 0, s1 = 0, s2 = 0;
-    for (int m = lane; m < a.nm; m += 32) {
-      double u = R[4 * m], v = R[4 * m + 1], wq = R[4 * m + 2];
-      d3 p;
-      double jac;
-      curved_point(Xn, u, v, p, jac);
-      double dx = X.x - p.x, dy = X.y - p.y, dz = X.z - p.z;
-      double r = sqrt(dx * dx + dy * dy + dz * dz);
-      double k = adl ? (dx * nx + dy * ny + dz * nz) / (r * r * r) : 1.0 / r;
-      k *= wq * jac * kInv4Pi;
-      s0 = fma(k, 1.0 - u - v, s0);
-      s1 = fma(k, u, s1);
-      s2 = fma(k, v, s2);
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // rows_per_warp > 1 (charge-reduce mode): the rows of one 32-row tile add
+  // into the tile's shared partial row, sequentially (deterministic order)
+  for (int w = wg * a.rows_per_warp; w < min(a.n_rows, (wg + 1) * a.rows_per_warp); ++w) {
+    const double* rd = a.rowdata + 6 * (size_t)w;
+    const d3 X = mk3(rd[0], rd[1], rd[2]);
+    const double nx = rd[3], ny = rd[4], nz = rd[5];
+    const bool adl = a.row_kind[w] == 1;
+    const int own = a.row_col[w];
+    const double sc = a.row_scale[w];
+    double* Arow = a.A + a.row_out[w];
+    if (own < 0) continue;
+    for (int s = a.vc_ptr[own]; s < a.vc_ptr[own + 1]; ++s) {
+      const int t = a.vc_tri[s], c = a.vc_corner[s];
+      const double* Xn = a.nodes6 + 18 * (size_t)t;
+      const double* R = a.rule + (size_t)c * a.nm * 4;
+      double s0 = 0, s1 = 0, s2 = 0;
+      for (int m = lane; m < a.nm; m += 32) {
+        double u = R[4 * m], v = R[4 * m + 1], wq = R[4 * m + 2];
+        d3 p;
+        double jac;
+        curved_point(Xn, u, v, p, jac);
+        double dx = X.x - p.x, dy = X.y - p.y, dz = X.z - p.z;
+        double r = sqrt(dx * dx + dy * dy + dz * dz);
+        double k = adl ? (dx * nx + dy * ny + dz * nz) / (r * r * r) : 1.0 / r;
+        k *= wq * jac * kInv4Pi;
+        s0 = fma(k, 1.0 - u - v, s0);
+        s1 = fma(k, u, s1);
+        s2 = fma(k, v, s2);
+      }
+      s0 = warp_sum(s0);
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        const int* tc = a.tri_cols + 3 * (size_t)t;
+        Arow[a.col_dev[tc[0]]] += sc * s0;
+        Arow[a.col_dev[tc[1]]] += sc * s1;
+        Arow[a.col_dev[tc[2]]] += sc * s2;
+      }
+      __syncwarp();
     }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    if (lane == 0) {
-      const int* tc = a.tri_cols + 3 * (size_t)t;
-      Arow[a.col_dev[tc[0]]] += sc * s0;
-      Arow[a.col_dev[tc[1]]] += sc * s1;
-      Arow[a.col_dev[tc[2]]] += sc * s2;
-    }
+    if (lane == 0) Arow[a.col_dev[own]] += a.row_diag[w];
     __syncwarp();
   }
-  if (lane == 0) Arow[a.col_dev[own]] += a.row_diag[w];
+}
+
+// K7 (charge / neutrality rows, reference charge_row src/assembly.py:540-569
+// and _row_equation 441-468): out[c] (+)= sum over the partial rows p (in
+// order) of part[p][c] -- the column sums of the charge-reduce sweep.
+__global__ void k_charge_reduce(const double* part, int n_parts, int64_t part_ld, int n, double* out,
+                                int accumulate) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double s = 0.0;
+  for (int p = 0; p < n_parts; ++p) s += part[(size_t)p * part_ld + c];
+  out[c] = accumulate ? out[c] + s : s;
 }
 
 // Columns n .. N-1 (floating potentials) of collocation rows: -1 in the
@@ -245,10 +261,18 @@ cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, 
   return cudaGetLastError();
 }
 
+cudaError_t launch_charge_reduce(const double* part, int n_parts, int64_t part_ld, int n, double* out, int accumulate,
+                                 cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_charge_reduce<<<(n + 255) / 256, 256, 0, st>>>(part, n_parts, part_ld, n, out, accumulate);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_singular(const SingularArgs& a, cudaStream_t st) {
   if (a.n_rows == 0) return cudaSuccess;
   int threads = 128;
-  int blocks = (a.n_rows * 32 + threads - 1) / threads;
+  const int items = (a.n_rows + a.rows_per_warp - 1) / a.rows_per_warp;
+  int blocks = (items * 32 + threads - 1) / threads;
   k_assemble_singular<<<blocks, threads, 0, st>>>(a);
   return cudaGetLastError();
 }
