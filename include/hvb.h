@@ -146,12 +146,17 @@ int hvb_gemv(const void* A, int prec, long long lda, int n_rows, int n_cols, con
 
 /* Fused GEMV + all-gather (row-sharded GMRES): as hvb_gemv
  * (f64), but each row result left[i] (A xp)_i is stored into all n_out
- * replicated vectors outs[k][out_off + i] -- this GPU's and every peer's,
- * mapped by CUDA IPC -- instead of a local y.  outs is a DEVICE array of
- * n_out pointers.  Replaces: matvec + the NCCL all-gather of the row
- * blocks (parallel.RowGather) */
+ * (= world) replicated vectors outs[k][out_off + i] -- this GPU's and every
+ * peer's, mapped by CUDA IPC -- instead of a local y; then the launch's
+ * last CTA publishes `epoch` into flags[r][rank] of every rank r with a
+ * system-scope release store (after system fences of every storing
+ * thread).  outs and flags are DEVICE arrays of n_out pointers; done is a
+ * zeroed device counter (reset by the kernel).  Pair with hvb_peer_wait.
+ * Replaces: matvec + the NCCL all-gather of the row blocks
+ * (parallel.RowGather) */
 int hvb_gemv_bcast(const double* A, long long lda, int n_rows, int n_cols, const double* x, const double* left,
-                   double* const* outs, int n_out, long long out_off, void* stream);
+                   double* const* outs, int n_out, long long out_off, unsigned long long* const* flags, int rank,
+                   unsigned long long epoch, unsigned int* done, void* stream);
 
 /* CUDA IPC plumbing for the peer buffers: a cudaMalloc'd (zeroed) region,
  * its handle (hvb_ipc_handle_bytes() bytes), and a peer's mapping. */
@@ -162,11 +167,10 @@ int hvb_ipc_handle(void* ptr, unsigned char* out);
 int hvb_ipc_open(const unsigned char* handle, void** ptr);
 int hvb_ipc_close(void* ptr);
 
-/* Cross-GPU epoch barrier over peer memory: signal writes `epoch` into slot
- * `rank` of every rank's flag row (flags: DEVICE array of world pointers),
- * after a system-scope fence; wait spins until every slot of this rank's
- * flag row reached `epoch`. */
-int hvb_peer_signal(unsigned long long* const* flags, int world, int rank, unsigned long long epoch, void* stream);
+/* Cross-GPU epoch barrier: spins (system-scope acquire loads) until every
+ * slot of this rank's flag row (DEVICE pointer, world slots) reached
+ * `epoch` -- the release stores of hvb_gemv_bcast; traps after ~17 s if a
+ * peer never signals. */
 int hvb_peer_wait(const unsigned long long* flags, int world, unsigned long long epoch, void* stream);
 
 /* xp[k] = z[perm[k]] / right[perm[k]]  (perm/right may be NULL) */

@@ -33,13 +33,12 @@ SIGNATURES = {
     "hvb_near_apply_rows": [_P, _I, _P, _P, _P, _P, _P, _P, _P, _P],
     "hvb_gemv": [_P, _I, _LL, _I, _I, _P, _P, _P, _P],
     "hvb_gather_scale": [_P, _P, _P, _I, _P, _P],
-    "hvb_gemv_bcast": [_P, _LL, _I, _I, _P, _P, _P, _I, _LL, _P],
+    "hvb_gemv_bcast": [_P, _LL, _I, _I, _P, _P, _P, _I, _LL, _P, _I, ctypes.c_ulonglong, _P, _P],
     "hvb_ipc_alloc": [_LL, _P],
     "hvb_ipc_free": [_P],
     "hvb_ipc_handle": [_P, _P],
     "hvb_ipc_open": [_P, _P],
     "hvb_ipc_close": [_P],
-    "hvb_peer_signal": [_P, _I, _I, ctypes.c_ulonglong, _P],
     "hvb_peer_wait": [_P, _I, ctypes.c_ulonglong, _P],
     "hvb_rowmax_diag": [_P, _I, _LL, _I, _I, _P, _P, _P, _P],
     "hvb_mgs": [_P, _LL, _I, _P, _I, _P, _P, _P, _I, _P],

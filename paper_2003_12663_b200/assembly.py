@@ -160,6 +160,7 @@ class RowBlock:
         self.stop = int(stop)
         self._data = None if data is None else np.asarray(data)
         self._store = store
+        self.version = 0  # bumped when ``data`` is replaced (SystemMatrix re-uploads)
 
     def __len__(self):
         return self.stop - self.start
@@ -174,6 +175,7 @@ class RowBlock:
     def data(self, value):
         self._data = np.asarray(value)
         self._store = None
+        self.version += 1
 
     @property
     def device_resident(self) -> bool:
@@ -222,7 +224,13 @@ class SystemMatrix:
         return matvec(self, v, workers=workers)
 
     def device_store(self) -> DeviceStore:
-        """The device copy (uploads host blocks once)."""
+        """The device copy.  Host-backed blocks are uploaded on first use and
+        again whenever a block's ``data`` was replaced since (the reference
+        reads the blocks on every call; an in-place edit of a block's array
+        needs ``invalidate()``)."""
+        stamp = tuple((id(b), b.version, id(b._data)) for b in self.blocks if not b.device_resident)
+        if self.store is not None and stamp and stamp != getattr(self, "_host_stamp", None):
+            self.store = None
         if self.store is None:
             import torch
 
@@ -233,7 +241,13 @@ class SystemMatrix:
             A = torch.zeros((self.size, lda), dtype=dt, device=dev)
             A[:, : self.size] = torch.as_tensor(data, dtype=dt, device=dev)
             self.store = DeviceStore(A, self.n, self.size, None, None)
+            self._host_stamp = stamp
         return self.store
+
+    def invalidate(self):
+        """Drop the device copy of host-backed blocks (re-uploaded on use)."""
+        if any(not b.device_resident for b in self.blocks):
+            self.store = None
 
 
 def _rowmax_diag(st: DeviceStore):

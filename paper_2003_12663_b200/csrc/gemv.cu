@@ -207,10 +207,39 @@ __global__ void k_rowmax_diag(const T* A, int64_t lda, int nrows, int ncols, con
   }
 }
 
+struct PeerSignal {
+  unsigned long long* const* flags;  // world pointers: flag row of every rank (null: no signal)
+  int world, rank;
+  unsigned long long epoch;
+  unsigned int* done;                // CTA completion counter (zero between launches)
+};
+
+// Release protocol of the fused GEMV + all-gather (csrc/peer.cu): every
+// thread that stored row results into peer memory fences at system scope,
+// the CTA barrier orders those fences before thread 0's completion count,
+// and the LAST CTA publishes the epoch into every rank's flag row with a
+// system-scope release store.  A peer that acquires the epoch
+// (hvb_peer_wait, ld.acquire.sys) therefore sees every row of this launch.
+HVB_DEV void peer_release(const PeerSignal& sig, int tid) {
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned prev = atomicAdd(sig.done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      for (int r = 0; r < sig.world; ++r) {
+        unsigned long long* f = sig.flags[r] + sig.rank;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(sig.epoch) : "memory");
+      }
+      *sig.done = 0u;  // stream order: the next launch starts from zero
+    }
+  }
+}
+
 template <int ROWS>
 __global__ void k_gemv_f64_v4(const double* __restrict__ A, int64_t lda, int nrows, int ncols,
                               const double* __restrict__ x, const double* __restrict__ left, double* __restrict__ y,
-                              double* const* outs, int n_out, int64_t out_off);
+                              double* const* outs, int n_out, int64_t out_off, PeerSignal sig);
 
 // 256-bit loads need 32-byte aligned rows and x: the production FP64 path
 // (2 rows per CTA, LDG.256 non-allocating: 7.5 TB/s on a cfg4-width block vs
@@ -233,7 +262,7 @@ cudaError_t launch_gemv(const void* A, int prec, int64_t lda, int nrows, int nco
                                                                         y);
   } else if (v4_ok(A, lda, x)) {
     k_gemv_f64_v4<2><<<(nrows + 1) / 2, GEMV_THREADS, 0, st>>>((const double*)A, lda, nrows, ncols, x, left, y,
-                                                               nullptr, 0, 0);
+                                                               nullptr, 0, 0, PeerSignal{});
   } else {
     constexpr int R = 4;
     k_gemv_f64<R><<<(nrows + R - 1) / R, GEMV_THREADS, 0, st>>>((const double*)A, lda, nrows, ncols, x, left, y,
@@ -243,16 +272,13 @@ cudaError_t launch_gemv(const void* A, int prec, int64_t lda, int nrows, int nco
 }
 
 cudaError_t launch_gemv_bcast(const double* A, int64_t lda, int nrows, int ncols, const double* x, const double* left,
-                              double* const* outs, int n_out, int64_t out_off, cudaStream_t st) {
-  if (nrows == 0) return cudaSuccess;
-  if (v4_ok(A, lda, x)) {
-    k_gemv_f64_v4<2><<<(nrows + 1) / 2, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, left, nullptr, outs, n_out,
-                                                               out_off);
-  } else {
-    constexpr int R = 4;
-    k_gemv_f64<R><<<(nrows + R - 1) / R, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, left, nullptr, outs, n_out,
-                                                                out_off);
-  }
+                              double* const* outs, int n_out, int64_t out_off, unsigned long long* const* flags,
+                              int rank, unsigned long long epoch, unsigned int* done, cudaStream_t st) {
+  // the row-sharded store is always 256-byte pitched; every rank owns >= 1 row
+  if (!v4_ok(A, lda, x) || nrows < 1) return cudaErrorInvalidValue;
+  PeerSignal sig{flags, n_out, rank, epoch, done};
+  k_gemv_f64_v4<2><<<(nrows + 1) / 2, GEMV_THREADS, 0, st>>>(A, lda, nrows, ncols, x, left, nullptr, outs, n_out,
+                                                             out_off, sig);
   return cudaGetLastError();
 }
 
@@ -515,11 +541,9 @@ namespace hvb {
 
 
 template <int ROWS>
-__global__ void k_gemv_f64_v4(const double* __restrict__ A, int64_t lda, int nrows,
-                                                              int ncols, const double* __restrict__ x,
-                                                              const double* __restrict__ left,
-                                                              double* __restrict__ y, double* const* outs, int n_out,
-                                                              int64_t out_off) {
+__global__ void k_gemv_f64_v4(const double* __restrict__ A, int64_t lda, int nrows, int ncols,
+                              const double* __restrict__ x, const double* __restrict__ left, double* __restrict__ y,
+                              double* const* outs, int n_out, int64_t out_off, PeerSignal sig) {
   const int r0 = blockIdx.x * ROWS;
   const int tid = threadIdx.x;
   double acc[ROWS];
@@ -564,7 +588,7 @@ __global__ void k_gemv_f64_v4(const double* __restrict__ A, int64_t lda, int nro
       y[r0 + tid] = v;
     }
   }
+  if (sig.flags) peer_release(sig, tid);
 }
-
 }  // namespace hvb
 

@@ -176,9 +176,12 @@ int hvb_gemv(const void* A, int prec, long long lda, int n_rows, int n_cols, con
 }
 
 int hvb_gemv_bcast(const double* A, long long lda, int n_rows, int n_cols, const double* x, const double* left,
-                   double* const* outs, int n_out, long long out_off, void* stream) {
-  if (n_out < 1 || out_off < 0) return fail(HVB_EARG, "hvb_gemv_bcast: bad n_out/out_off");
-  return check(hvb::launch_gemv_bcast(A, lda, n_rows, n_cols, x, left, outs, n_out, out_off, (cudaStream_t)stream),
+                   double* const* outs, int n_out, long long out_off, unsigned long long* const* flags, int rank,
+                   unsigned long long epoch, unsigned int* done, void* stream) {
+  if (n_out < 1 || n_out > 32 || out_off < 0 || rank < 0 || rank >= n_out || n_rows < 1 || !flags || !done)
+    return fail(HVB_EARG, "hvb_gemv_bcast: bad n_out/out_off/rank/n_rows or missing flags/counter");
+  return check(hvb::launch_gemv_bcast(A, lda, n_rows, n_cols, x, left, outs, n_out, out_off, flags, rank, epoch, done,
+                                      (cudaStream_t)stream),
                "hvb_gemv_bcast");
 }
 
@@ -207,11 +210,6 @@ int hvb_ipc_open(const unsigned char* handle, void** ptr) {
 }
 
 int hvb_ipc_close(void* ptr) { return check(cudaIpcCloseMemHandle(ptr), "hvb_ipc_close"); }
-
-int hvb_peer_signal(unsigned long long* const* flags, int world, int rank, unsigned long long epoch, void* stream) {
-  if (world < 1 || world > 32 || rank < 0 || rank >= world) return fail(HVB_EARG, "hvb_peer_signal: bad world/rank");
-  return check(hvb::launch_peer_signal(flags, world, rank, epoch, (cudaStream_t)stream), "hvb_peer_signal");
-}
 
 int hvb_peer_wait(const unsigned long long* flags, int world, unsigned long long epoch, void* stream) {
   if (world < 1 || world > 32) return fail(HVB_EARG, "hvb_peer_wait: bad world");

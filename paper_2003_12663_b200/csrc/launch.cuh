@@ -107,9 +107,8 @@ cudaError_t launch_near_apply_rows(const int* seg_ptr, int n_seg, const int* pai
 cudaError_t launch_gemv(const void* A, int prec, int64_t lda, int nrows, int ncols, const double* x,
                         const double* left, double* y, cudaStream_t st);
 cudaError_t launch_gemv_bcast(const double* A, int64_t lda, int nrows, int ncols, const double* x, const double* left,
-                              double* const* outs, int n_out, int64_t out_off, cudaStream_t st);
-cudaError_t launch_peer_signal(unsigned long long* const* flags, int world, int rank, unsigned long long epoch,
-                               cudaStream_t st);
+                              double* const* outs, int n_out, int64_t out_off, unsigned long long* const* flags,
+                              int rank, unsigned long long epoch, unsigned int* done, cudaStream_t st);
 cudaError_t launch_peer_wait(const unsigned long long* flags, int world, unsigned long long epoch, cudaStream_t st);
 cudaError_t launch_gather_scale(const double* z, const double* right, const int* perm, int n, double* xp,
                                 cudaStream_t st);

@@ -21,6 +21,7 @@ PAPER.md:203 distributes the same row blocks over GPUs.  Here block b of
 
 from __future__ import annotations
 
+import ctypes
 import logging
 import os
 
@@ -83,62 +84,119 @@ class _CudaArray:
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
 
 
+def _release_region(base, opened):
+    """Finalizer of a PeerGather: unmap the peers' regions, free ours."""
+    from . import _lib
+
+    for p in opened:
+        try:
+            _lib.call("hvb_ipc_close", ctypes.c_void_p(p))
+        except Exception:  # noqa: BLE001 - interpreter teardown
+            pass
+    try:
+        _lib.call("hvb_ipc_free", ctypes.c_void_p(base))
+    except Exception:  # noqa: BLE001
+        pass
+
+
+def _agree(ok: bool, group, device) -> bool:
+    """True on every rank iff ``ok`` on every rank (all_reduce MIN)."""
+    import torch
+    import torch.distributed as dist
+
+    on_dev = dist.get_backend(group) == "nccl"
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device if on_dev else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return bool(flag.item())
+
+
 class PeerGather:
     """Fused GEMV + all-gather over CUDA IPC peer memory (csrc/peer.cu).
 
     Every rank owns a cudaMalloc'd region -- two replicated N-vectors
-    (alternating by epoch parity) and a row of `world` epoch flags -- and
-    maps every peer's region.  One matvec = hvb_gemv_bcast (each row result
-    stored into all replicas over NVLink) + hvb_peer_signal + hvb_peer_wait;
-    no NCCL call and no separate gather launch on the data path."""
+    (alternating by epoch parity), a row of `world` epoch flags and the GEMV's
+    CTA completion counter -- and maps every peer's region.  One matvec =
+    hvb_gemv_bcast (each row result stored into all replicas over NVLink,
+    the last CTA release-stores the epoch into every rank's flag row) +
+    hvb_peer_wait (acquire); no NCCL call and no separate gather launch on
+    the data path.  Build with ``PeerGather.create``: every rank takes the
+    peer path or none does (the IPC setup outcome is agreed by all_reduce
+    before anyone uses it); the region is released by a finalizer."""
 
-    def __init__(self, total: int, group=None, device=None):
-        import ctypes
-
-        import torch
+    @classmethod
+    def create(cls, total: int, group=None, device=None):
         import torch.distributed as dist
 
         from . import _lib
 
-        self.group = group
+        self = cls.__new__(cls)
+        self.group, self.device, self.total = group, device, total
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.total = total
-        self.device = device
-        h = _lib.lib()
         vec_bytes = 8 * total
-        region = 2 * vec_bytes + 8 * self.world
+        self._vec_bytes = vec_bytes
+        region = 2 * vec_bytes + 8 * self.world + 64
         base = ctypes.c_void_p()
-        _lib.call("hvb_ipc_alloc", region, ctypes.byref(base))
-        self._base = base.value
-        hb = h.hvb_ipc_handle_bytes()
-        handle = (ctypes.c_ubyte * hb)()
-        _lib.call("hvb_ipc_handle", ctypes.c_void_p(self._base), handle)
+        handle = None
+        try:
+            _lib.call("hvb_ipc_alloc", region, ctypes.byref(base))
+            hb = _lib.lib().hvb_ipc_handle_bytes()
+            handle = (ctypes.c_ubyte * hb)()
+            _lib.call("hvb_ipc_handle", base, handle)
+            ok = True
+        except Exception as exc:  # noqa: BLE001 - reported, then agreed across ranks
+            logger.warning("peer-memory region unavailable on rank %d (%s)", self.rank, exc)
+            ok = False
+        if not _agree(ok, group, device):
+            if base.value:
+                _release_region(base.value, [])
+            return None
         handles = [None] * self.world
         dist.all_gather_object(handles, bytes(handle), group=group)
-        bases, self._opened = [], []
+        bases, opened = [], []
+        ok = True
         for r, hd in enumerate(handles):
             if r == self.rank:
-                bases.append(self._base)
+                bases.append(base.value)
                 continue
-            buf = (ctypes.c_ubyte * hb).from_buffer_copy(hd)
+            buf = (ctypes.c_ubyte * len(hd)).from_buffer_copy(hd)
             p = ctypes.c_void_p()
-            _lib.call("hvb_ipc_open", buf, ctypes.byref(p))
+            try:
+                _lib.call("hvb_ipc_open", buf, ctypes.byref(p))
+            except Exception as exc:  # noqa: BLE001
+                logger.warning("rank %d cannot map rank %d's region (%s)", self.rank, r, exc)
+                ok = False
+                break
             bases.append(p.value)
-            self._opened.append(p.value)
-        i64 = dict(dtype=torch.int64, device=device)
-        self.vec_ptrs = [torch.tensor([b + par * vec_bytes for b in bases], **i64) for par in (0, 1)]
-        self.flag_ptrs = torch.tensor([b + 2 * vec_bytes for b in bases], **i64)
-        self.my_flags = self._base + 2 * vec_bytes
-        self.local = [torch.as_tensor(_CudaArray(self._base + par * vec_bytes, total), device=device)
-                      for par in (0, 1)]
-        self.epoch = 0
+            opened.append(p.value)
+        if not _agree(ok, group, device):
+            _release_region(base.value, opened)
+            return None
+        self._init_views(base.value, bases, opened)
         dist.barrier(group=group)  # every peer has mapped every region
+        return self
+
+    def _init_views(self, base, bases, opened):
+        import weakref
+
+        import torch
+
+        vb = self._vec_bytes
+        self._base = base
+        i64 = dict(dtype=torch.int64, device=self.device)
+        self.vec_ptrs = [torch.tensor([b + par * vb for b in bases], **i64) for par in (0, 1)]
+        self.flag_ptrs = torch.tensor([b + 2 * vb for b in bases], **i64)
+        self.my_flags = base + 2 * vb
+        self.done_ptr = base + 2 * vb + 8 * self.world
+        self.local = [torch.as_tensor(_CudaArray(base + par * vb, self.total), device=self.device) for par in (0, 1)]
+        self.epoch = 0
+        self._finalizer = weakref.finalize(self, _release_region, base, list(opened))
+
+    def close(self):
+        self._finalizer()
 
     def matvec(self, store, row0: int, z, right, left_local):
         """Full y = left .* A (z ./ right) from this rank's row block."""
-        import ctypes
-
         from . import _lib
         from .assembly import gather_operand
 
@@ -147,8 +205,8 @@ class PeerGather:
         par = self.epoch & 1
         s = _lib.stream_ptr(self.device)
         _lib.call("hvb_gemv_bcast", _lib.ptr(store.A), store.lda, int(store.A.shape[0]), store.size, _lib.ptr(xp),
-                  _lib.ptr(left_local), _lib.ptr(self.vec_ptrs[par]), self.world, row0, s)
-        _lib.call("hvb_peer_signal", _lib.ptr(self.flag_ptrs), self.world, self.rank, self.epoch, s)
+                  _lib.ptr(left_local), _lib.ptr(self.vec_ptrs[par]), self.world, row0, _lib.ptr(self.flag_ptrs),
+                  self.rank, self.epoch, ctypes.c_void_p(self.done_ptr), s)
         _lib.call("hvb_peer_wait", ctypes.c_void_p(self.my_flags), self.world, self.epoch, s)
         return self.local[par].clone()
 
@@ -163,15 +221,7 @@ class _DistOperator:
         self.device = dmat.device
         self.size = dmat.size
         self.gather = RowGather(dmat.size, dmat.group)
-        self.peer = None
-        st = dmat.store
-        if (_peer_gather_enabled() and st is not None and not st.is_f32 and dmat._apply is None
-                and self.device is not None and self.device.type == "cuda"):
-            try:
-                self.peer = PeerGather(dmat.size, dmat.group, self.device)
-            except Exception as exc:  # IPC unavailable: the NCCL all-gather path
-                logger.warning("peer-memory gather unavailable (%s); using the NCCL all-gather", exc)
-                self.peer = None
+        self.peer = dmat.peer_gather()
         global LAST_GATHER
         LAST_GATHER = "peer" if self.peer is not None else "collective"
 
@@ -222,6 +272,18 @@ class DistributedMatrix:
         if self._rowmax is not None:
             return self._rowmax()
         return _rowmax_diag(self.store)
+
+    def peer_gather(self):
+        """The matrix's PeerGather (built once, on the first solve), or None
+        when every rank agreed on the NCCL all-gather (HVB_PEER_GATHER=0,
+        float32 storage, CPU operator, or IPC setup failed on some rank)."""
+        if not hasattr(self, "_peer"):
+            st = self.store
+            usable = (_peer_gather_enabled() and st is not None and not st.is_f32 and self._apply is None
+                      and self.device is not None and self.device.type == "cuda")
+            # every rank evaluates the same conditions; create() agrees on IPC itself
+            self._peer = PeerGather.create(self.size, self.group, self.device) if usable else None
+        return self._peer
 
     def operator(self):
         return _DistOperator(self)

@@ -80,9 +80,10 @@ def test_distributed_gmres_matches_single(N):
     assert abs(it0 - it) <= 1
 
 
-def _gpu_worker(rank, world, port, out_q):
+def _gpu_worker(rank, world, port, out_q, peer="1"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["HVB_PEER_GATHER"] = peer
     dist.init_process_group("gloo", rank=rank, world_size=world)  # ranks share cuda:0 here
     try:
         torch.cuda.set_device(0)
@@ -145,6 +146,37 @@ def test_row_sharded_device_path_matches_single_process():
     for g, ln in zip(got, lines):
         assert g.shape == ln.points.shape
         np.testing.assert_allclose(g, ln.points, rtol=0, atol=1e-10)
+
+
+def _run_pair(target, *extra):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, 2, port, q, *extra)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in procs], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")
+def test_peer_gather_equals_nccl_gather_bitwise():
+    """The fused GEMV + peer-memory all-gather (release/acquire epoch flags,
+    csrc/peer.cu) and the collective all-gather path (HVB_PEER_GATHER=0)
+    give bitwise-identical solves, fields and lines (2 ranks on cuda:0)."""
+    peer = _run_pair(_gpu_worker, "1")
+    coll = _run_pair(_gpu_worker, "0")
+    assert [r[5] for r in peer] == ["peer", "peer"] and [r[5] for r in coll] == ["collective", "collective"]
+    for a, b in zip(peer, coll):
+        np.testing.assert_array_equal(a[1], b[1])
+        assert a[2] == b[2]
+        np.testing.assert_array_equal(a[3], b[3])
+        for pa, pb in zip(a[4], b[4]):
+            np.testing.assert_array_equal(pa, pb)
 
 
 def _float_worker(rank, world, port, out_q):

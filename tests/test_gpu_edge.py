@@ -239,3 +239,37 @@ def test_mgs_matches_host_gram_schmidt(n, j):
     run(0, w2, h2)
     run(1, w2, h2)
     assert torch.equal(w2, w) and torch.equal(h2, h)
+
+
+def test_host_block_replacement_reuploads():
+    """A host-backed SystemMatrix re-uploads a block whose data was replaced
+    (the reference reads its blocks on every matvec)."""
+    from paper_2003_12663_b200.assembly import RowBlock, SystemMatrix, matvec
+
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((6, 6))
+    m = SystemMatrix(n=6, n_floating=0, blocks=[RowBlock(0, 3, A[:3].copy()), RowBlock(3, 6, A[3:].copy())])
+    v = rng.standard_normal(6)
+    np.testing.assert_allclose(matvec(m, v), A @ v, rtol=1e-13)
+    B = rng.standard_normal((3, 6))
+    m.blocks[1].data = B
+    np.testing.assert_allclose(matvec(m, v), np.concatenate([A[:3] @ v, B @ v]), rtol=1e-13)
+
+
+def test_field_sources_follow_in_place_density_edits(cases):
+    """Editing solution.u in place (past index 2) re-uploads u AND rebuilds
+    the density-contracted sources: the far field and the near pass both
+    use the new density (a stale source cache mixed densities)."""
+    from paper_2003_12663_b200.assembly import assemble
+    from paper_2003_12663_b200.postprocess import eval_efield_batch
+    from paper_2003_12663_b200.solver import Solution, SolverConfig, solve
+
+    m = cases("cap2")
+    A, rhs = assemble(m)
+    sol = solve(A, rhs, SolverConfig(rel_tol=1e-12))
+    P = np.array([[0.7, 0.1, 0.05], [0.0, 0.62, 0.1]])
+    eval_efield_batch(sol, m, P)
+    sol.u[7:] *= 1.5
+    got = eval_efield_batch(sol, m, P)
+    fresh = eval_efield_batch(Solution(u=sol.u.copy(), V=sol.V, iterations=0, residual=0.0), m, P)
+    np.testing.assert_array_equal(got, fresh)

@@ -106,45 +106,6 @@ def test_solver_config_validation():
 # ---------------------------------------------------------------------------
 
 
-@pytest.mark.parametrize("maker,window,strips", [
-    (lambda: fixtures.sphere_mesh(3), 64, True),
-    (lambda: fixtures.close_gap_mesh(2), 96, False),
-    (lambda: fixtures.rod_plane_mesh(0.15), 64, True),
-])
-def test_column_tiling_invariants(maker, window, strips):
-    from paper_2003_12663_b200.device import column_tiling
-
-    m = maker()
-    T = column_tiling(m.colloc_points, m.tri_corner_cols, max_tile=4096, band_max=window - 32, strips=strips)
-    n = m.n_collocation
-    assert sorted(T.perm.tolist()) == list(range(n))
-    assert np.array_equal(T.inv[T.perm], np.arange(n))
-    assert T.tile_width.sum() == n and np.all(np.diff(T.tile_col0) == T.tile_width[:-1])
-    # every (panel, corner) is owned by exactly one entry; one primary entry per panel
-    owned = np.zeros((m.n_triangles, 3), dtype=int)
-    prim = np.zeros(m.n_triangles, dtype=int)
-    for k in range(len(T.tile_width)):
-        a, b = T.tile_ptr[k], T.tile_ptr[k + 1]
-        meta = T.ent_meta[a:b]
-        tri = T.ent_tri[a:b]
-        assert np.all(np.diff(meta[:, 0]) >= 0)  # sorted by first owned column
-        for e in range(b - a):
-            t = tri[e]
-            for c in range(3):
-                l = meta[e, 1 + c]
-                if l >= 0:
-                    owned[t, c] += 1
-                    # the owned local column is the corner's device column
-                    assert T.inv[m.tri_corner_cols[t, c]] == T.tile_col0[k] + l
-        prim[tri] += meta[:, 4]
-        # pair band fits the window
-        for e in range(0, b - a, 2):
-            grp = meta[e:e + 2, 1:4]
-            assert grp[grp >= 0].max() - meta[e, 0] <= window - 32
-    assert np.all(owned == 1)
-    assert np.all(prim == 1)
-
-
 # ---------------------------------------------------------------------------
 # quadrature (reference tests/test_quadrature.py semantics)
 # ---------------------------------------------------------------------------
@@ -434,17 +395,18 @@ def test_import_alias_drop_in():
         sys.modules.update(saved)
 
 
-@pytest.mark.parametrize("scale", [0.12, 0.4])
-def test_column_tiling_invariants(scale):
+@pytest.mark.parametrize("maker", [lambda: fixtures.sphere_mesh(3), lambda: fixtures.close_gap_mesh(2),
+                                   lambda: fixtures.rod_plane_mesh(0.12), lambda: fixtures.rod_plane_mesh(0.4)])
+def test_column_tiling_invariants(maker):
     """csrc/tiling.cpp (host C++, no GPU): the device column order is a
     permutation; every (panel, tile owning one of its corners) record exists
     once with its owned corners; stages of 4 records have pairwise disjoint
     owned columns within the 32-column band of their first record, whose
     first owned column is the stage minimum; stage starts never decrease
     within a tile; dummies (-1) only pad stages."""
-    from paper_2003_12663_b200 import device, fixtures
+    from paper_2003_12663_b200 import device
 
-    m = fixtures.rod_plane_mesh(scale)
+    m = maker()
     T = device.column_tiling(m.colloc_points, m.tri_corner_cols, max_tile=2048)
     n = m.n_collocation
     assert np.array_equal(np.sort(T.perm), np.arange(n))
