@@ -18,9 +18,16 @@ H2D, u and E D2H inside the timed region).
 
 Prints ONE JSON line (rank 0).  ``value`` = assembly entries/s (N^2 / max
 over ranks of the assembly time); GMRES solve seconds and field evals/s are
-reported beside it.  ``--impl reference`` times the CPU oracle port of the
-reference (oracle/, the reference is pure Python and cannot be installed on
-the box) on a bounded sample of the same workload with all host cores.
+reported beside it; the full config-5 trace (every collocation vertex seeded,
+~1e5 lines) is timed once after the steps (``trace_full``).
+
+``--impl reference`` times the reference's OWN implementation, hvbem 0.1.0
+as installed unmodified into baseline/_ref (pip --target), on
+the box's host cores: per step, reference ``_row_equation`` on a bounded
+sample of evenly spaced config-4 rows over a fork pool of every core
+(entries/s = rows x N / time); once, the reference ``matvec`` on a row-block
+sample and ``eval_efield`` at one point per core.  When baseline/_ref is
+missing it falls back to the oracle port (oracle/, kind "port").
 """
 
 from __future__ import annotations
@@ -51,6 +58,8 @@ def parse():
     ap.add_argument("--points", type=int, default=100_000, help="field points per step (whole job)")
     ap.add_argument("--lines", type=int, default=8192, help="cfg5 field lines per step (whole job; 0 = skip)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-full-trace", dest="full_trace", action="store_false",
+                    help="skip the once-per-run config-5 trace of every vertex (~1e5 lines)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--cpu-rows", type=int, default=24, help="cpu_baseline sample rows")
     return ap.parse_args()
@@ -112,6 +121,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def measured_copy_gbs():
+    """The driver-measured copy bandwidth (MEASURED_PEAKS.json hbm_gbs)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def measure_peaks(dev):
     """DFMA throughput and read-stream bandwidth of this GPU (denominators)."""
     import torch
@@ -158,7 +176,6 @@ def regular_flops(mesh, near_rows_counts, sl_rows, adl_rows):
 # ---------------------------------------------------------------------------
 
 _CPU_MESH = None
-EVALS_PER_LINE = 140.2  # field evaluations per traced cfg5 line (B200 run, tools/trace_probe.py 1.0 100000)
 
 
 _CPU_TABLES = None
@@ -241,12 +258,9 @@ def cpu_sample(mesh, n_rows: int, processes: int, field_points: int = 4):
         "t_rows": t_rows,
         "matvec_s": t_mv,
         "field_evals_per_s": evals_per_s,
-        # a traced line costs ~EVALS_PER_LINE field evaluations (measured on
-        # the B200 cfg5 run; the surface-distance queries are ~1 % on top)
-        "trace_lines_per_s": evals_per_s / EVALS_PER_LINE,
         "sample": (f"oracle port: {n_rows} evenly spaced cfg4 rows (row_equations, {processes} procs) "
                    f"-> entries/s x N; numpy GEMV on a 4096-row block; E at {field_points} points "
-                   f"({min(processes, field_points)} procs); lines/s = evals/s / {EVALS_PER_LINE} (extrapolated)"),
+                   f"({min(processes, field_points)} procs)"),
     }
 
 
@@ -259,39 +273,180 @@ def _cpu_field(P):
     ora.efield_points(_CPU_MESH, np.ones(_CPU_MESH.n_collocation), P)
 
 
-def run_reference(args):
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+_REF = {}
+
+
+def _ref_rows(rows):
+    """Forked worker: the reference's own _row_equation on `rows`."""
+    _one_thread()
+    ra, cfg, mesh, tab = _REF["assembly"], _REF["cfg"], _REF["mesh"], _REF["tables"]
+    t = time.perf_counter()
+    for r in rows:
+        ra._row_equation(mesh, cfg, tab, int(r))
+    return time.perf_counter() - t
+
+
+def _ref_field(x):
+    _one_thread()
+    t = time.perf_counter()
+    _REF["post"].eval_efield(_REF["solution"], _REF["mesh"], x, _REF["cfg"])
+    return time.perf_counter() - t
+
+
+def _load_reference(scale):
+    """The reference package from baseline/_ref and its own parse of the
+    config-4 mesh (text written by our generator, parsed by hvbem.mesh)."""
+    import importlib
+
     import numpy as np
 
+    sys.path.insert(0, REF_DIR)
+    try:
+        rmesh = importlib.import_module("hvbem.mesh")
+        ra = importlib.import_module("hvbem.assembly")
+        rpost = importlib.import_module("hvbem.postprocess")
+        rsol = importlib.import_module("hvbem.solver")
+        rq = importlib.import_module("hvbem.quadrature")
+    finally:
+        sys.path.pop(0)
+    if not os.path.dirname(os.path.abspath(rmesh.__file__)).startswith(REF_DIR):
+        raise ImportError("hvbem imported from outside baseline/_ref")
+    from paper_2003_12663_b200 import fixtures
+
+    v, ids, tags, lines = fixtures.rod_plane_parts(scale)
+    t0 = time.perf_counter()
+    text = fixtures.mesh_text(v, [(tuple(r), int(g)) for r, g in zip(ids.tolist(), tags.tolist())], lines)
+    mesh = rmesh.parse_mesh(text)
+    cfg = rq.QuadConfig()
+    tab = mesh.tables(cfg.regular_order)
+    _REF.update(assembly=ra, post=rpost, mesh=mesh, cfg=cfg, tables=tab,
+                solution=rsol.Solution(u=np.ones(mesh.n_collocation), V=np.zeros(0), iterations=0, residual=0.0),
+                setup_s=time.perf_counter() - t0, matvec=ra.matvec, RowBlock=ra.RowBlock, SystemMatrix=ra.SystemMatrix)
+    return mesh
+
+
+def reference_sample(mesh, cores: int, warmup: int, steps: int):
+    """The reference's own code on the host cores (fork pool, one BLAS
+    thread per process): entries/s of _row_equation on 2 x cores evenly
+    spaced rows per step (median of `steps` after `warmup`), eval_efield at
+    one point per core, and one reference matvec on a row-block sample
+    extrapolated to N rows."""
+    import multiprocessing as mp
+
+    import numpy as np
+
+    n = mesh.n_collocation
+    N = n + mesh.n_floating
+    per_step = 2 * cores                       # rows per step: ~0.1 s of CPU work per row at config 4
+    vals = []
+    with mp.get_context("fork").Pool(cores) as pool:
+        for k in range(warmup + steps):
+            rows = np.minimum(np.linspace(0, n - 1, per_step).astype(int) + k % 7, n - 1)
+            t0 = time.perf_counter()
+            pool.map(_ref_rows, [rows[i::cores].tolist() for i in range(cores)])
+            dt = time.perf_counter() - t0
+            if k >= warmup:
+                vals.append(per_step * N / dt)
+        # field evaluation: one point per core (reference eval_efield)
+        rng = np.random.default_rng(0)
+        lo, hi = mesh.vertices.min(axis=0), mesh.vertices.max(axis=0)
+        P = 0.5 * (lo + hi) + rng.uniform(-0.6, 0.6, (cores, 3)) * (hi - lo)
+        t0 = time.perf_counter()
+        pool.map(_ref_field, list(P))
+        evals_per_s = cores / (time.perf_counter() - t0)
+    # GMRES matvec: the reference's matvec on a row-block sample, blocks over
+    # its own thread pool (workers = cores), extrapolated to N rows
+    rows_blk = min(N, 64 * cores)
+    blocks = [_REF["RowBlock"](a, b, np.random.default_rng(a).standard_normal((b - a, N)))
+              for a, b in _partition(rows_blk, cores)]
+    mat = _REF["SystemMatrix"](n=N, n_floating=0, blocks=blocks)
+    x = np.random.default_rng(1).standard_normal(N)
+    _REF["matvec"](mat, x, workers=cores)
+    t0 = time.perf_counter()
+    _REF["matvec"](mat, x, workers=cores)
+    matvec_s = (time.perf_counter() - t0) * N / rows_blk
+    del blocks, mat
+    return {"entries_per_s": float(np.median(vals)), "field_evals_per_s": evals_per_s, "matvec_s": matvec_s,
+            "sample": (f"hvbem 0.1.0 from baseline/_ref: _row_equation on {per_step} evenly spaced cfg4 rows per "
+                       f"step over {cores} forked processes (entries/s = rows x N / time, median of {steps}); "
+                       f"matvec on a {rows_blk}-row block (workers={cores}) x N/{rows_blk}; eval_efield at "
+                       f"{cores} points (one per process)")}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own code (baseline/_ref) on the host
+    cores; the oracle port stands in only if baseline/_ref is missing."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    cores = os.cpu_count() or 1
+    try:
+        mesh = _load_reference(args.scale)
+    except ImportError as exc:
+        sys.stderr.write(f"baseline/_ref unavailable ({exc}); timing the oracle port\n")
+        return _run_port_reference(args, cores)
+    N = mesh.n_collocation + mesh.n_floating
+    smp = reference_sample(mesh, cores, args.warmup, args.steps)
+    v = smp["entries_per_s"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "entries/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": N * N / v * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (deterministic rod-plane generator; mesh parsed by the reference's own parse_mesh)",
+        "config": {"workload": f"cfg4 rod-plane+insulator: {mesh.n_triangles} panels, N={N}",
+                   "panels": mesh.n_triangles, "N": N},
+        "gmres_solve_s": None,
+        "gmres_matvec_s": smp["matvec_s"],
+        "field_evals_per_s": smp["field_evals_per_s"],
+        "reference_setup_s": _REF["setup_s"],
+        "cpu_baseline": {"value": v, "unit": "entries/s", "cores": cores, "kind": "reference",
+                         "sample": smp["sample"]},
+        "e2e": {"value": v, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": ("extrapolated from row samples: the full cfg4 system is 79 GB (no CPU assembly or GMRES solve "
+                 "at this size; gmres_matvec_s is one reference matvec, iterations are set by the matrix)"),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _partition(total, parts):
+    q, r = divmod(total, parts)
+    out, a = [], 0
+    for b in range(parts):
+        e = a + q + (1 if b < r else 0)
+        if e > a:
+            out.append((a, e))
+        a = e
+    return out
+
+
+def _run_port_reference(args, cores):
+    import numpy as np
+
     from paper_2003_12663_b200 import fixtures
 
     mesh = fixtures.rod_plane_mesh(args.scale)
     N = mesh.n_collocation + mesh.n_floating
-    cores = os.cpu_count() or 1
-    vals = []
-    samp = None
+    vals, samp = [], None
     for k in range(args.warmup + args.steps):
         s = cpu_sample(mesh, max(4 * cores, args.cpu_rows), cores, field_points=max(2, cores))
         if k >= args.warmup:
             vals.append(s)
         samp = s
-    v = float(np.median([s["entries_per_s"] for s in vals])) if vals else samp["entries_per_s"]
-    iters = 74  # reference GMRES iterations on cfg4 (measured with the same semantics on B200)
+    v = float(np.median([s["entries_per_s"] for s in vals]))
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "entries/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": N * N / v * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (deterministic rod-plane generator)",
-        "config": {"workload": f"cfg4 rod-plane+insulator {mesh.n_triangles} panels N={N}", "panels": mesh.n_triangles,
-                   "N": N},
-        "gmres_solve_s": float(np.median([s["matvec_s"] for s in vals])) * (iters + 3),
+        "config": {"workload": f"cfg4 rod-plane+insulator: {mesh.n_triangles} panels, N={N}",
+                   "panels": mesh.n_triangles, "N": N},
+        "gmres_solve_s": None,
+        "gmres_matvec_s": float(np.median([s["matvec_s"] for s in vals])),
         "field_evals_per_s": float(np.median([s["field_evals_per_s"] for s in vals])),
-        "trace": {"lines_per_s": float(np.median([s["trace_lines_per_s"] for s in vals])),
-                  "note": "extrapolated: field evals/s / evals per line"},
         "cpu_baseline": {"value": v, "unit": "entries/s", "cores": cores, "kind": "port", "sample": samp["sample"]},
         "e2e": {"value": v, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "baseline/_ref missing: the oracle port (oracle/hvb_oracle.py) stands in for the reference",
     }
     print(json.dumps(line), flush=True)
 
@@ -331,7 +486,10 @@ def run_b200(args):
     from paper_2003_12663_b200.solver import SolverConfig, solve
 
     tflops_peak, read_gbs = measure_peaks(dev)
+    copy_gbs = measured_copy_gbs()
+    t_mb = time.perf_counter()
     mesh = fixtures.rod_plane_mesh(args.scale)
+    mesh_build_s = time.perf_counter() - t_mb
     n, nt = mesh.n_collocation, mesh.n_triangles
     N = n + mesh.n_floating
     rng = np.random.default_rng(1234)
@@ -381,6 +539,7 @@ def run_b200(args):
         res = tracer.trace_device(sol, mesh, starts[la:lb], orient, postprocess.TraceParams(), QuadConfig())
         val, ver = tracer.streamer_device(res, gas)
         trace_stats.update(rounds=res.rounds, evals=res.field_points, lines=lb - la,
+                           accepted=int((res.info[:, 0] - 1).sum()) if lb > la else 0,
                            inception=int(ver.sum().item()),
                            terms=np.bincount(res.info[:, 1], minlength=4).tolist(),
                            max_points=int(res.info[:, 0].max()) if lb > la else 0)
@@ -497,21 +656,60 @@ def run_b200(args):
     del A, st
     torch.cuda.empty_cache()
 
-    # end to end through the public API from host buffers
+    # full config 5: every collocation vertex seeded (~1e5 lines), traced once
+    trace_full = None
+    if args.full_trace and args.lines > 0:
+        trace_stats.clear()
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        t0e.record()
+        saved = args.lines
+        args.lines = n
+        trace_phase(sol)
+        args.lines = saved
+        t1e.record()
+        barrier()
+        tf = t0e.elapsed_time(t1e) / 1e3
+        vec = torch.tensor([tf, trace_stats.get("evals", 0), trace_stats.get("inception", 0),
+                            trace_stats.get("accepted", 0)], dtype=torch.float64, device=dev)
+        if world > 1:
+            t_only = vec[:1].clone()
+            dist.all_reduce(t_only, op=dist.ReduceOp.MAX)
+            dist.all_reduce(vec)
+            vec[0] = t_only[0]
+        tf, evals_f, inc_f, acc_f = vec.tolist()
+        # a field evaluation is 9 nt (classification) + 12 x 17 nt
+        # (density-contracted E nodes) flop, near pairs and the surface
+        # distance on top (not counted)
+        fl = evals_f * (9.0 + 12 * 17) * nt
+        trace_full = {"lines": n, "seconds": tf, "lines_per_s": n / tf, "field_evals": int(evals_f),
+                      "evals_per_line": evals_f / n, "reference_scheme_evals_per_line": (evals_f + acc_f) / n,
+                      "inception_lines": int(inc_f), "achieved_tflops": fl / tf / 1e12,
+                      "frac_of_fp64_peak": fl / tf / 1e12 / tflops_peak,
+                      "rank0_terminations": dict(zip(("SurfaceHit", "WeakField", "MaxLength", "LeftDomain"),
+                                                     trace_stats.get("terms", []))),
+                      "note": "config 5 at its size: seeds at every collocation vertex (0.25 local R along the "
+                              "normal), orientation sign(E.n), device RK45 + streamer; timed once after the steps; "
+                              "the reference scheme needs one more evaluation per accepted step"}
+
+    # end to end through the public API from host buffers, E2E_REPS times
+    # (median): every mesh-derived product -- the column tiling, the device
+    # buffers (H2D), the kd-tree of the coincidence check -- is rebuilt from
+    # the host SurfaceMesh inside the timed region, exactly as assemble() on
+    # a freshly loaded mesh does; u and E come back to the host.  Building
+    # the SurfaceMesh itself (the reference's parse_mesh) is timed apart.
     e2e = None
     if not args.no_e2e:
-        # the pass through the public API from host buffers, E2E_REPS times
-        # (median): every device buffer of the mesh is rebuilt from the host
-        # arrays (H2D) inside the timed region; host-side mesh-derived arrays
-        # (column tiling, vertex kd-tree) stay, like circumcentres; u and E
-        # come back to the host
+        from paper_2003_12663_b200.device import mesh_tiling
+
         reps = []
         for _ in range(E2E_REPS):
             barrier()
+            mesh._device_cache.clear()
             t0 = time.perf_counter()
-            for k in [k for k in mesh._device_cache if isinstance(k, tuple) and k[0] == "dm"]:
-                del mesh._device_cache[k]
-            device_mesh(mesh)  # (also done inside assemble; split out for the breakdown)
+            mesh_tiling(mesh)  # (also done inside assemble; split out for the breakdown)
+            t_tile = time.perf_counter()
+            device_mesh(mesh)
             torch.cuda.synchronize(dev)
             t_dm = time.perf_counter()
             if world > 1:
@@ -526,27 +724,39 @@ def run_b200(args):
             E = postprocess.eval_efield_batch(sol, mesh, P_all[pa:pb])
             torch.cuda.synchronize(dev)
             t3 = time.perf_counter()
-            reps.append([t1 - t0, t2 - t1, t3 - t2, t_dm - t0])
-        ea, es, ef, eu = np.median(np.array(reps), axis=0).tolist()
+            reps.append([t1 - t0, t2 - t1, t3 - t2, t_tile - t0, t_dm - t_tile])
+        ea, es, ef, et, eu = np.median(np.array(reps), axis=0).tolist()
         dmh = device_mesh(mesh)
         h2d = dmh.h2d_bytes + P_dev.numel() * 8 + N * 8  # mesh + tiling arrays, field points, rhs
         d2h = int(n * 8 + E.size * 8)
-        evec = torch.tensor([ea, es, ef, eu], dtype=torch.float64, device=dev)
+        evec = torch.tensor([ea, es, ef, et, eu], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(evec, op=dist.ReduceOp.MAX)
-        ea, es, ef, eu = evec.tolist()
+        ea, es, ef, et, eu = evec.tolist()
         e2e = {"value": N * N / ea, "unit": "entries/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "gmres_solve_s": es, "field_evals_per_s": args.points / ef,
-               "breakdown_s": {"device_mesh_upload": eu, "assemble": ea - eu}, "reps": E2E_REPS,
-               "note": "public API from host mesh arrays; device mesh rebuilt (H2D) inside the timed region; "
-                       "median of reps"}
+               "breakdown_s": {"column_tiling": et, "device_mesh_upload": eu, "assemble": ea - et - eu,
+                               "solve": es, "field": ef},
+               "mesh_build_s": mesh_build_s, "reps": E2E_REPS,
+               "note": "public API from the host SurfaceMesh: column tiling (host C++), device mesh (H2D), "
+                       "assembly, solve and E at the field points each rep, u and E read back; median of reps; "
+                       "the SurfaceMesh construction (mesh_build_s) is reported apart"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        s = cpu_sample(mesh, args.cpu_rows, 1, field_points=2)
-        cpu = {"value": s["entries_per_s"], "unit": "entries/s", "cores": 1, "kind": "port",
+        # the reference's own code (baseline/_ref) on every host core; the
+        # oracle port stands in if baseline/_ref is missing
+        cores = os.cpu_count() or 1
+        try:
+            _load_reference(args.scale)
+            s, kind = reference_sample(_REF["mesh"], cores, 1, 3), "reference"
+        except ImportError:
+            s, kind = cpu_sample(mesh, max(args.cpu_rows, 2 * cores), cores, field_points=cores), "port"
+        epl = trace_full["reference_scheme_evals_per_line"] if trace_full else None
+        cpu = {"value": s["entries_per_s"], "unit": "entries/s", "cores": cores, "kind": kind,
                "sample": s["sample"], "matvec_s": s["matvec_s"], "field_evals_per_s": s["field_evals_per_s"],
-               "trace_lines_per_s": s["trace_lines_per_s"]}
+               "trace_lines_per_s": (s["field_evals_per_s"] / epl) if epl else None,
+               "trace_note": "field evals/s / the reference scheme's evaluations per line measured in trace_full"}
 
     if rank == 0:
         line = {
@@ -575,6 +785,7 @@ def run_b200(args):
                                    "note": "every collocation point + 0.25 local R along its normal (SURVEY 8d)"},
             "phases_s": {"assembly": t_asm, "solve": t_solve, "field": t_field, "trace": t_trace,
                          "assembly_regular_kernel": reg_t},
+            "trace_full": trace_full,
             "trace": {"lines": min(args.lines, n), "lines_per_s": min(args.lines, n) / t_trace if t_trace else None,
                       "field_evals": int(trace_evals), "inception_lines": int(trace_inception),
                       "rank0_rounds": trace_stats.get("rounds"), "rank0_terminations": dict(zip(
@@ -587,7 +798,8 @@ def run_b200(args):
                          "traffic": _ncu_traffic("k_sweep"), "peak_source": "measured DFMA kernel on this GPU (hvb_bench_dfma)"},
             "roofline_gemv": {"bound": "hbm", "kernel": "k_gemv_f64", "traffic": _ncu_traffic("k_gemv"), "achieved": gemv_bytes / t_gemv / 1e9,
                               "peak": read_gbs, "unit": "GB/s", "frac": gemv_bytes / t_gemv / 1e9 / read_gbs,
-                              "frac_of_measured_copy": gemv_bytes / t_gemv / 1e9 / 6547.2,
+                              "frac_of_measured_copy": (gemv_bytes / t_gemv / 1e9 / copy_gbs) if copy_gbs else None,
+                              "measured_copy_gbs": copy_gbs,
                               "ms_per_matvec": t_gemv * 1e3,
                               "peak_source": "measured read-stream kernel on this GPU (hvb_bench_read: 256-bit non-allocating loads)"},
             "gpu_launches": launches,

@@ -1,5 +1,6 @@
 """The bench contract on CPU: `bench.py --impl reference` (the reference arm:
-the oracle port timed on the host cores) prints one JSON line with the
+the reference's own hvbem from baseline/_ref timed on the host cores, the
+oracle port when baseline/_ref is absent) prints one JSON line with the
 metric, unit, cpu_baseline and e2e keys the driver reads."""
 
 import json
@@ -23,7 +24,8 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["metric"] == base["metric"]
     assert d["unit"] == "entries/s" and d["higher_is_better"] is True and d["value"] > 0
     cb = d["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    want = "reference" if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "hvbem")) else "port"
+    assert cb["kind"] == want and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"] == {"value": d["value"], "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
 
 
