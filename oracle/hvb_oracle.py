@@ -404,7 +404,11 @@ def entry_error(a, b, floor=1e-4):
 # ---------------------------------------------------------------------------
 
 
-def gmres(A, b, restart=100, rel_tol=1e-8, max_iters=2000, row_equilibrate=True):
+def gmres(A, b, restart=100, rel_tol=1e-8, max_iters=2000, row_equilibrate=True, matvec=None):
+    """``matvec`` (optional) replaces A @ z in the operator and the true
+    residual -- e.g. the reference's float32 row dots for single storage
+    (assembly.py:386-392); row scales and the diagonal come from A."""
+    mv = matvec or (lambda z: np.asarray(A, dtype=float) @ z)
     A = np.asarray(A, dtype=float)
     b = np.asarray(b, dtype=float)
     N = len(b)
@@ -417,10 +421,10 @@ def gmres(A, b, restart=100, rel_tol=1e-8, max_iters=2000, row_equilibrate=True)
         return np.zeros(N), 0, 0.0
 
     def op(z):
-        return left * (A @ (z / right))
+        return left * mv(z / right)
 
     def tres(x):
-        return np.linalg.norm(b - A @ x) / nb
+        return np.linalg.norm(b - mv(x)) / nb
 
     x = np.zeros(N)
     it = 0

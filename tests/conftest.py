@@ -10,6 +10,11 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.npz")
 
+# the reference's own test modules (vendored verbatim, tools/vendor_reference_tests.sh)
+# import `hvbem`: they run in a subprocess behind the import alias
+# (tests/test_reference_suite.py), never in this session
+collect_ignore = ["reference_suite"]
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libhvb.so")

@@ -266,3 +266,28 @@ def test_floating_conductor_gate_opt_in():
     sol = solve(A, rhs, SolverConfig(true_residual_gate=False))
     assert np.max(np.abs(sol.u - x[: m.n_collocation])) <= 1e-6 * np.max(np.abs(x))
     assert abs(sol.V[0] - x[-1]) <= 1e-6 * abs(x[-1])
+
+
+def test_case_outputs_bitwise_across_blockings(cases, tmp_path):
+    """solution.json and surface_field.csv from the device path are
+    byte-identical for any row blocking (reference
+    tests/test_cli.py:96-108: workers {1, 4}, blocks 3)."""
+    from paper_2003_12663_b200 import outputs
+    from paper_2003_12663_b200.assembly import assemble
+    from paper_2003_12663_b200.config import Config
+    from paper_2003_12663_b200.postprocess import surface_field_magnitudes
+    from paper_2003_12663_b200.solver import solve
+
+    m = cases("diel2")
+    got = []
+    for blocks in (1, 3):
+        out = tmp_path / f"b{blocks}"
+        out.mkdir()
+        A, rhs = assemble(m, n_blocks=blocks)
+        sol = solve(A, rhs)
+        e = surface_field_magnitudes(m, sol)
+        outputs.write_solution(out, "/case/mesh.bemesh", m, sol, e, Config(), {}, 1, blocks)
+        outputs.write_surface_csv(out / "surface_field.csv", m, e)
+        got.append(out)
+    for name in ("solution.json", "surface_field.csv"):
+        assert (got[0] / name).read_bytes() == (got[1] / name).read_bytes()

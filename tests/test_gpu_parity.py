@@ -166,15 +166,45 @@ def test_gemv_host_matrix():
         assert np.max(np.abs(y - a @ v)) <= 1e-13 * max(1.0, np.max(np.abs(a @ v)))
 
 
-def test_single_precision_storage(cases):
+def test_single_precision_storage_reference_semantics(cases, monkeypatch):
+    """precision="single" (reference src/assembly.py:482-484, 386-392): the
+    stored matrix is the float64 one rounded to float32; matvec casts v to
+    float32 and reduces every row in float32 like the reference's
+    ``data[i] @ vc`` -- checked against that exact numpy float32 dot within
+    the float32 summation-order bound; GMRES on the single matrix agrees
+    with the oracle GMRES run on the same float32 matvec semantics; the
+    opt-in double-sum reduction is at least as close to the exact product."""
+    from oracle import hvb_oracle as ora
+    from paper_2003_12663_b200 import assembly
     from paper_2003_12663_b200.assembly import assemble, matvec
+    from paper_2003_12663_b200.solver import SolverConfig, solve
 
-    m = cases("sphere2")
-    A32, _ = assemble(m, precision="single")
+    m = cases("diel2")
+    A32, rhs = assemble(m, precision="single")
+    a32 = A32.toarray()
     assert A32.blocks[0].data.dtype == np.float32
-    A64, _ = assemble(m)
-    v = np.ones(m.n_collocation)
-    assert np.max(np.abs(matvec(A32, v) - matvec(A64, v))) <= 1e-5
+    np.testing.assert_array_equal(a32, assemble(m)[0].toarray().astype(np.float32))
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal(A32.size)
+    v32 = v.astype(np.float32)
+    ref = np.array([a32[i] @ v32 for i in range(A32.size)], dtype=np.float64)  # the reference's float32 dot
+    exact = a32.astype(np.float64) @ v32.astype(np.float64)
+    mag = np.abs(a32).astype(np.float64) @ np.abs(v32).astype(np.float64)
+    eps32 = np.finfo(np.float32).eps
+    y = matvec(A32, v)
+    bound = 2 * np.sqrt(A32.size) * eps32 * mag  # two float32 summation orders of N terms
+    assert np.all(np.abs(y - ref) <= bound)
+    assert np.max(np.abs(y - exact) / mag) > 1e-10  # really float32 sums, not double
+    monkeypatch.setattr(assembly, "SINGLE_SUMS_F64", True)
+    y64 = matvec(A32, v)
+    assert np.max(np.abs(y64 - exact) / mag) <= np.max(np.abs(y - exact) / mag)
+    monkeypatch.setattr(assembly, "SINGLE_SUMS_F64", False)
+    sol = solve(A32, rhs, SolverConfig(rel_tol=1e-5))
+    x, it, _ = ora.gmres(a32, rhs, rel_tol=1e-5,
+                         matvec=lambda z: (a32 @ z.astype(np.float32)).astype(np.float64))
+    full = np.concatenate([sol.u, sol.V])
+    assert np.max(np.abs(full - x)) <= 1e-3 * np.max(np.abs(x))
+    assert abs(sol.iterations - it) <= 2
 
 
 def test_assemble_vs_oracle_random_points(cases):

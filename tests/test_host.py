@@ -374,7 +374,7 @@ def test_import_alias_drop_in():
     saved = {k: v for k, v in sys.modules.items() if k == "hvbem" or k.startswith("hvbem.")}
     try:
         sys.modules["hvbem"] = importlib.import_module("paper_2003_12663_b200")
-        for sub in ("mesh", "quadrature", "kernels", "assembly", "solver", "postprocess", "fixtures", "config"):
+        for sub in ("mesh", "quadrature", "kernels", "assembly", "solver", "postprocess", "fixtures", "config", "cli"):
             sys.modules[f"hvbem.{sub}"] = importlib.import_module(f"paper_2003_12663_b200.{sub}")
         from hvbem.assembly import (KERNEL_ADL, KERNEL_SL, AssemblyError, RowBlock, SystemMatrix,  # noqa: F401
                                     assemble, assemble_kernel_row, charge_row, load_matrix, matvec,
@@ -440,3 +440,41 @@ def test_column_tiling_invariants(maker):
                 seen.add((t, k))
     want = {(t, int(tile_of[c])) for t in range(m.n_triangles) for c in m.tri_corner_cols[t]}
     assert seen == want
+
+
+# ---------------------------------------------------------------------------
+# case outputs (reference src/cli.py:172-235): byte-compatible writers
+# ---------------------------------------------------------------------------
+
+
+def test_case_outputs_match_reference_bytes(tmp_path):
+    """solution.json, surface_field.csv and surface_field.vtk written by
+    paper_2003_12663_b200.outputs equal, byte for byte, the files the
+    reference's own writers produced on the same inputs
+    (tests/golden/make_outputs_golden.py), and load_solution reads them."""
+    import importlib.util
+
+    from paper_2003_12663_b200 import outputs
+    from paper_2003_12663_b200.config import Config
+    from paper_2003_12663_b200.solver import Solution
+
+    spec = importlib.util.spec_from_file_location("mog", os.path.join(ROOT, "tests", "golden",
+                                                                       "make_outputs_golden.py"))
+    src = open(spec.origin).read()
+    ns = {}
+    exec(src[src.index("MESH_PATH ="):src.index('if __name__ == "__main__":')], {"np": np}, ns)
+    mesh = fixtures.sphere_mesh(1)
+    u, e = ns["inputs"](mesh.n_collocation)
+    sol = Solution(u=u, V=np.zeros(0), iterations=7, residual=3.25e-9)
+    outputs.write_solution(tmp_path, ns["MESH_PATH"], mesh, sol, e, Config(), {"total": 1.0}, 1, 1)
+    outputs.write_surface_csv(tmp_path / "surface_field.csv", mesh, e)
+    outputs.write_surface_vtk(tmp_path / "surface_field.vtk", mesh, e)
+    gold = os.path.join(ROOT, "tests", "golden", "outputs")
+    for name in ("solution.json", "surface_field.csv", "surface_field.vtk"):
+        assert (tmp_path / name).read_bytes() == open(os.path.join(gold, name), "rb").read(), name
+    doc, back = outputs.load_solution(gold)
+    assert doc["format"] == outputs.SOLUTION_FORMAT and back.iterations == 7
+    np.testing.assert_array_equal(back.u, u)
+    with pytest.raises(ValueError, match="unknown solution format"):
+        (tmp_path / "solution.json").write_text('{"format": "x"}')
+        outputs.load_solution(tmp_path)

@@ -11,7 +11,7 @@ cat > "$ALIAS/sitecustomize.py" <<PY
 import importlib, sys
 sys.path.insert(0, "$ROOT")
 sys.modules["hvbem"] = importlib.import_module("paper_2003_12663_b200")
-for sub in ("mesh", "quadrature", "kernels", "assembly", "solver", "postprocess", "fixtures", "config"):
+for sub in ("mesh", "quadrature", "kernels", "assembly", "solver", "postprocess", "fixtures", "config", "cli"):
     sys.modules[f"hvbem.{sub}"] = importlib.import_module(f"paper_2003_12663_b200.{sub}")
 PY
 files=("$@")
