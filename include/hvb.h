@@ -50,6 +50,10 @@ int hvb_build_stream(const double* table, int nq, const double* ccr, double eta,
                      const int* ent_meta, long long n_entries, int mode, int window, double* stream_out,
                      void* stream);
 int hvb_stream_record_doubles(int nq, int mode);
+/* Regular-sweep geometry of this build (HOST pointer out[4]): window
+ * columns, flush width, records per stage, window row stride (doubles).
+ * The host tiling uses band = window - flush and stages of that size. */
+int hvb_sweep_geometry(int* out);
 
 /* Column tiling of the regular sweep (HOST function, host pointers; no
  * GPU needed; csrc/tiling.cpp): recursive coordinate bisection of the n

@@ -31,24 +31,41 @@
 
 #include "launch.cuh"
 
+// Geometry (compile-time; hvb_sweep_geometry reports it to the host, which
+// builds the tiling with band = WIN - FLUSH and stages of R records).
+#ifndef HVB_SWEEP_WIN
+#define HVB_SWEEP_WIN 64
+#endif
+#ifndef HVB_SWEEP_WPC
+#define HVB_SWEEP_WPC 4
+#endif
+#ifndef HVB_SWEEP_MINB
+#define HVB_SWEEP_MINB 3
+#endif
+
 namespace hvb {
 namespace sweep {
 constexpr int ROWS = 32;
 constexpr int STRIDE = 33;
-constexpr int WIN = 48;                                  // window columns
+constexpr int WIN = HVB_SWEEP_WIN;                       // window columns
 constexpr int SLOTS = WIN + 1;                           // + dump slot
 constexpr int WREG = (SLOTS * STRIDE + 1) & ~1;          // doubles per warp window (16-byte aligned)
 constexpr int FLUSH = 16;                                // columns per flush (band <= WIN - FLUSH)
 constexpr int R = 4;                                     // records per stage
-constexpr int WPC = 8;                                   // warps per CTA
+constexpr int WPC = HVB_SWEEP_WPC;                       // warps per CTA
+constexpr int MINB = HVB_SWEEP_MINB;                     // resident CTAs per SM (register budget)
+constexpr size_t kSmemBudget = 232448;                   // 227 KB per SM usable by CTAs
 
 template <int NQ, int MODE>
 struct Rec {
   static constexpr int NQP = MODE == 0 ? (NQ + 1) & ~1 : NQ;  // SL: node pairs (odd NQ padded)
   static constexpr int DOUBLES = (MODE == 0 ? 5 : 6) * NQP + 8;
   static constexpr int TAIL = DOUBLES - 8;
-  // ring stages: as many as fit two 8-warp CTAs per SM (228 KB) for NQ = 12
-  static constexpr int S = DOUBLES <= 72 ? 4 : 3;
+  // ring stages: as many (<= 4) as fit MINB CTAs per SM
+  static constexpr size_t kWin = (size_t)WPC * WREG * 8;
+  static constexpr size_t kStage = (size_t)R * DOUBLES * 8 + 16;
+  static constexpr int kFit = (int)((kSmemBudget / MINB - 1024 - kWin) / kStage);
+  static constexpr int S = kFit > 4 ? 4 : (kFit < 2 ? 2 : kFit);
 };
 
 HVB_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -79,16 +96,12 @@ HVB_DEV void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar
       : "memory");
 }
 
-// one (row, record) classification: regular iff ||x - cc|| > fl(eta R),
-// decided as the reference rounds it.  sq is the 3-op FMA sum of squares
-// (within 4 ulp of the unfused sum, far inside the bracket's 1e-13 margins,
-// so the bracket decides as the unfused sum would); only a pair inside the
-// bracket pays for the unfused sum and the IEEE sqrt.
-HVB_DEV bool regular(d3 d, double sq, const double* tail) {
-  bool r = sq > tail[5];
-  if (!r && !(sq < tail[4])) r = __dsqrt_rn(sumsq_unfused(d)) > tail[3];
-  return r;
-}
+// hat_c(q) of the regular rule per nq in {3, 6, 12, 16} (index 0..3):
+// constant bank operands of the SL node FMAs (uploaded once per device by
+// launch_regular; the values depend on nq only)
+__constant__ double c_hats[4][16][3];
+
+__host__ __device__ constexpr int hat_index(int nq) { return nq == 3 ? 0 : nq == 6 ? 1 : nq == 12 ? 2 : 3; }
 }  // namespace sweep
 
 // RED (charge-reduce mode, MODE 1 only): instead of one row per lane, the
@@ -96,7 +109,7 @@ HVB_DEV bool regular(d3 d, double sq, const double* tail) {
 // the tile's partial row a.A + tile * a.part_ld (csrc/tables.cu
 // k_charge_reduce then sums the partial rows in order).
 template <int NQ, int MODE, bool RED = false>
-__global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
+__global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularArgs a) {
   using namespace sweep;
   using RC = Rec<NQ, MODE>;
   constexpr int REC = RC::DOUBLES;
@@ -195,7 +208,7 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
     // the classification, the window byte offsets of its corners
     d3 xc[R];
     double sq[R];
-    bool reg[R], emit[R];
+    bool reg[R], amb[R], emit[R];
     int tris[R];
     unsigned slw[R], sfw[R];  // packed window byte offsets (+ flags)
     bool any_emit = false;
@@ -204,11 +217,25 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
       const double* tl = pr + j * REC + RC::TAIL;
       xc[j] = sub_rn(X0, mk3(tl[0], tl[1], tl[2]));
       sq[j] = fma(xc[j].z, xc[j].z, fma(xc[j].y, xc[j].y, xc[j].x * xc[j].x));
-      reg[j] = sweep::regular(xc[j], sq[j], tl);
+      // classification: regular iff ||x - cc|| > fl(eta R), decided as the
+      // reference rounds it.  sq is the 3-op FMA sum of squares (within 4 ulp
+      // of the unfused sum, far inside the bracket's 1e-13 margins, so the
+      // bracket decides as the unfused sum would); pairs inside the bracket
+      // are settled below with the unfused sum and the IEEE sqrt
+      reg[j] = sq[j] > tl[5];
+      amb[j] = !reg[j] && !(sq[j] < tl[4]);
       const int* meta = reinterpret_cast<const int*>(tl + 6);
       slw[j] = static_cast<unsigned>(meta[2]);
       sfw[j] = static_cast<unsigned>(meta[3]);
       tris[j] = meta[0];
+    }
+    if (__any_sync(0xffffffffu, amb[0] || amb[1] || amb[2] || amb[3])) {  // rare: one uniform branch per stage
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if (amb[j]) reg[j] = __dsqrt_rn(sumsq_unfused(xc[j])) > pr[j * REC + RC::TAIL + 3];
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
       emit[j] = !reg[j] && ((sfw[j] >> 16) & 1u) && live0;  // from the panel's primary tile only
       any_emit |= emit[j];
     }
@@ -232,8 +259,8 @@ __global__ void __launch_bounds__(32 * sweep::WPC, 2) k_sweep(RegularArgs a) {
           const double k1 = rsqrt2_newton(r1);
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            acc[j][c] = fma(k0, a.hats[q][c], acc[j][c]);
-            acc[j][c] = fma(k1, a.hats[q + 1][c], acc[j][c]);
+            acc[j][c] = fma(k0, c_hats[hat_index(NQ)][q][c], acc[j][c]);
+            acc[j][c] = fma(k1, c_hats[hat_index(NQ)][q + 1][c], acc[j][c]);
           }
         }
       }
@@ -352,6 +379,13 @@ static cudaError_t launch_sweep_nq(const RegularArgs& a, cudaStream_t st) {
 
 int sweep_window_stride() { return sweep::STRIDE; }
 
+void sweep_geometry(int* out) {
+  out[0] = sweep::WIN;
+  out[1] = sweep::FLUSH;
+  out[2] = sweep::R;
+  out[3] = sweep::STRIDE;
+}
+
 int sweep_record_doubles(int nq, int mode) {
   switch (nq) {
     case 3: return mode == 0 ? sweep::Rec<3, 0>::DOUBLES : sweep::Rec<3, 1>::DOUBLES;
@@ -365,6 +399,19 @@ int sweep_record_doubles(int nq, int mode) {
 // mode 0: SL rows (SL record stream), 1: ADL rows (ADL record stream)
 cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, cudaStream_t st) {
   if (a.n_rows <= 0 || a.n_tiles <= 0) return cudaSuccess;
+  if (mode == 0) {  // the rule's hat values into constant memory, once per (device, nq)
+    static bool done[64][4];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const int hi = sweep::hat_index(nq);
+    if (dev < 64 && !done[dev][hi]) {
+      e = cudaMemcpyToSymbol(sweep::c_hats, a.hats, sizeof(a.hats), (size_t)hi * sizeof(a.hats),
+                             cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return e;
+      done[dev][hi] = true;
+    }
+  }
   auto go = [&](auto nq_tag) -> cudaError_t {
     constexpr int Q = decltype(nq_tag)::value;
     if (a.part_ld > 0) return launch_sweep_nq<Q, 1, true>(a, st);

@@ -60,6 +60,12 @@ int hvb_build_stream(const double* table, int nq, const double* ccr, double eta,
 
 int hvb_stream_record_doubles(int nq, int mode) { return hvb::sweep_record_doubles(nq, mode); }
 
+int hvb_sweep_geometry(int* out) {
+  if (!out) return fail(HVB_EARG, "hvb_sweep_geometry: null output");
+  hvb::sweep_geometry(out);
+  return HVB_OK;
+}
+
 int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_col0,
                          const int* tile_width, int n_tiles, int nq, const double* hats, int row_begin, int n_rows,
                          const double* rowdata, const int* row_col, const double* row_scale,

@@ -88,6 +88,7 @@ struct FieldArgs {
 cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, cudaStream_t st);
 int sweep_record_doubles(int nq, int mode);
 int sweep_window_stride();
+void sweep_geometry(int* out);
 cudaError_t launch_build_table(const double* nodes6, int nt, int nq, const double* rule, double* out,
                                cudaStream_t st);
 cudaError_t launch_build_stream(const double* table, int nq, const double* ccr, double eta, const int* ent_tri,

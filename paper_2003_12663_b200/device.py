@@ -9,7 +9,7 @@ Host side (NumPy, once per mesh):
   corners of every aligned group of GROUP consecutive records lie within
   ``band`` columns of the group's first owned column, which is what lets
   the assembly warp keep a WINDOW-column sliding window of running sums
-  (csrc/assemble.cu: WINDOW 48, flushes of 16 columns, band 32).
+  (csrc/assemble.cu, sweep_geometry(): WINDOW 48, flushes of 16 columns, band 32).
   Panels with corners in several tiles are evaluated once per tile
   (``redundancy``, 1.14 at config 4).
 * entries (tile, panel) sorted by (tile, first owned column).
@@ -31,16 +31,27 @@ import numpy as np
 from . import _lib
 from .quadrature import QuadConfig, duffy_rule, graded_rule, regular_rule
 
-__all__ = ["ColumnTiling", "column_tiling", "DeviceMesh", "device_mesh", "WINDOW"]
+__all__ = ["ColumnTiling", "column_tiling", "DeviceMesh", "device_mesh", "sweep_geometry"]
 
-# regular-sweep geometry (csrc/assemble.cu): a 48-column window per warp,
-# flushed 16 columns at a time, so the panel band over every aligned group of
-# GROUP = 4 records (one bulk-copy stage) must stay within WINDOW - FLUSH = 32
-# columns.  Measured on cfg4 in round 1: 48 columns beat 40/44/56/64.
-WINDOW = 48
-FLUSH = 16
-GROUP = 4
 MAX_TILE = 32767
+
+
+def sweep_geometry():
+    """(window, flush, group, stride) of the built regular sweep
+    (csrc/assemble.cu, hvb_sweep_geometry): a WINDOW-column window per warp
+    flushed FLUSH columns at a time, so the owned corners of every stage of
+    GROUP records must lie within band = WINDOW - FLUSH columns."""
+    global _GEOM
+    if _GEOM is None:
+        import ctypes
+
+        out = (ctypes.c_int * 4)()
+        _lib.call("hvb_sweep_geometry", out)
+        _GEOM = tuple(int(v) for v in out)
+    return _GEOM
+
+
+_GEOM = None
 
 
 @dataclass
@@ -56,8 +67,8 @@ class ColumnTiling:
     redundancy: float
 
 
-def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = MAX_TILE, band_max: int = WINDOW - FLUSH,
-                  group: int = GROUP) -> ColumnTiling:
+def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = MAX_TILE, band_max: int | None = None,
+                  group: int | None = None) -> ColumnTiling:
     """Column tiles + grouped (tile, panel) records, built natively
     (csrc/tiling.cpp, host C++): recursive coordinate bisection into tiles
     of <= max_tile columns swept along their longest axis; records sorted by
@@ -68,6 +79,9 @@ def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = MAX_
     direction.  ``redundancy`` = real records per panel."""
     import ctypes
 
+    win, flush, grp, _ = sweep_geometry()
+    band_max = win - flush if band_max is None else band_max
+    group = grp if group is None else group
     pts = np.ascontiguousarray(points, dtype=np.float64)
     tc = np.ascontiguousarray(tri_cols, dtype=np.int32)
     n, nt = len(pts), len(tc)
@@ -159,7 +173,7 @@ class DeviceMesh:
                   _lib.ptr(self.table), st)
 
         # column tiling + panel streams
-        self.window = WINDOW
+        self.window, _, _, self.window_stride = sweep_geometry()
         tiling = mesh_tiling(mesh, max_tile)
         self.tiling = tiling
         self.perm = up(tiling.perm, **i32)
@@ -190,7 +204,7 @@ class DeviceMesh:
             st = torch.empty((self.n_entries, rec), dtype=torch.float64, device=self.device)
             with torch.cuda.device(self.device):
                 _lib.call("hvb_build_stream", _lib.ptr(self.table), self.nq, _lib.ptr(self.ccr), float(self.cfg.eta),
-                          _lib.ptr(self._ent_tri), _lib.ptr(self._ent_meta), self.n_entries, mode, WINDOW,
+                          _lib.ptr(self._ent_tri), _lib.ptr(self._ent_meta), self.n_entries, mode, self.window,
                           _lib.ptr(st), _lib.stream_ptr(self.device))
             self._streams[mode] = st
         return st
@@ -224,7 +238,7 @@ def panel_groups(cc: np.ndarray, radii: np.ndarray, thr: np.ndarray) -> np.ndarr
 
 def mesh_tiling(mesh, max_tile: int = MAX_TILE) -> ColumnTiling:
     """Column tiling of a mesh (a mesh-derived array, cached on it)."""
-    key = ("tiling", max_tile, WINDOW, FLUSH, GROUP)
+    key = ("tiling", max_tile) + sweep_geometry()
     cache = mesh._device_cache
     t = cache.get(key)
     if t is None:

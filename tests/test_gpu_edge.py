@@ -176,7 +176,7 @@ def test_device_panel_data_matches_host_statement(maker):
         assert np.array_equal(rec[real][:, -8:-5], m.circumcenters[ent])
         tail = np.ascontiguousarray(rec[:, -2:])
         offs = tail.view(np.uint16).reshape(len(rec), 8)[:, 4:7].astype(np.int64)
-        assert np.array_equal(offs, np.where(loc >= 0, loc % dm.window, dm.window) * 33 * 8)  # 33: window stride
+        assert np.array_equal(offs, np.where(loc >= 0, loc % dm.window, dm.window) * dm.window_stride * 8)
         flags = tail.view(np.uint16).reshape(len(rec), 8)[:, 7]
         assert not np.any(flags[~real])
     # SL stream nodes: x'.Y + |x'|^2 Q + P = |x - y|^2 / w^2 (csrc/assemble.cu)

@@ -400,13 +400,16 @@ def test_import_alias_drop_in():
 def test_column_tiling_invariants(maker):
     """csrc/tiling.cpp (host C++, no GPU): the device column order is a
     permutation; every (panel, tile owning one of its corners) record exists
-    once with its owned corners; stages of 4 records have pairwise disjoint
-    owned columns within the 32-column band of their first record, whose
+    once with its owned corners; stages of `group` records have pairwise
+    disjoint owned columns within the band (window - flush) of their first
+    record, whose
     first owned column is the stage minimum; stage starts never decrease
     within a tile; dummies (-1) only pad stages."""
     from paper_2003_12663_b200 import device
 
     m = maker()
+    win, flush, grp, _ = device.sweep_geometry()
+    band = win - flush
     T = device.column_tiling(m.colloc_points, m.tri_corner_cols, max_tile=2048)
     n = m.n_collocation
     assert np.array_equal(np.sort(T.perm), np.arange(n))
@@ -416,10 +419,10 @@ def test_column_tiling_invariants(maker):
     seen = set()
     for k in range(len(T.tile_width)):
         a, b = int(T.tile_ptr[k]), int(T.tile_ptr[k + 1])
-        assert (b - a) % 4 == 0
+        assert (b - a) % grp == 0
         prev = -1
-        for s0 in range(a, b, 4):
-            st = range(s0, s0 + 4)
+        for s0 in range(a, b, grp):
+            st = range(s0, s0 + grp)
             cols = [c for e in st for c in T.ent_meta[e, 1:4] if c >= 0]
             assert len(cols) == len(set(cols))                       # disjoint owned corners
             start = T.ent_meta[s0, 0]
@@ -431,7 +434,7 @@ def test_column_tiling_invariants(maker):
                     assert np.all(T.ent_meta[e, 1:4] == -1) and T.ent_meta[e, 4] == 0
                     continue
                 own = [c for c in T.ent_meta[e, 1:4] if c >= 0]
-                assert min(own) == T.ent_meta[e, 0] >= start and max(own) <= start + 32
+                assert min(own) == T.ent_meta[e, 0] >= start and max(own) <= start + band
                 corners = m.tri_corner_cols[t]
                 exp = [int(local[c]) if tile_of[c] == k else -1 for c in corners]
                 assert list(T.ent_meta[e, 1:4]) == exp
