@@ -43,6 +43,7 @@ HVB_DEV void field_tile(const FieldArgs& a, int bx, int by, double2* s_src, doub
   const int lane = tid & 31;
   const int ti = bx * FT + tid;
   const bool live = ti < a.m;
+  const bool warp_live = bx * FT + (tid & ~31) < a.m;
   const int tt = live ? ti : a.m - 1;
   const d3 X = mk3(a.pts[3 * (size_t)tt], a.pts[3 * (size_t)tt + 1], a.pts[3 * (size_t)tt + 2]);
   const int own = a.own_col ? a.own_col[tt] : -1;
@@ -60,6 +61,9 @@ HVB_DEV void field_tile(const FieldArgs& a, int bx, int by, double2* s_src, doub
     for (int k = tid; k < cn * 6; k += FT) s_cls[k] = a.cls[(size_t)c0 * 6 + k];
     for (int k = tid; k < cn * 3; k += FT) s_cols[k] = a.tri_cols[(size_t)c0 * 3 + k];
     __syncthreads();
+    // a warp whose 32 targets are all past the count only helps stage the
+    // chunk (the tracer's tail rounds have a handful of live targets per CTA)
+    if (!warp_live) continue;
     // whole group far from the target: every panel is regular (exactly;
     // device.py panel_groups) -- skip the per-panel classification
     const double* gb = a.groups + 8 * (size_t)(c0 / FCH);
@@ -157,37 +161,43 @@ __global__ void __launch_bounds__(FT) k_field_dyn(FieldArgs a, unsigned long lon
   }
 }
 
-// fixed-order reduction of the panel splits, count on the device
-__global__ void k_field_reduce_dyn(const double* part, int split, const unsigned long long* m_dev, double* out) {
-  const int m = (int)*m_dev;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    double s0 = 0, s1 = 0, s2 = 0;
-    for (int s = 0; s < split; ++s) {
-      const double* p = part + ((size_t)s * m + i) * 4;
-      s0 += p[0];
-      s1 += p[1];
-      s2 += p[2];
-    }
+// Fixed-order reduction of the panel splits: one warp per target, lane l
+// sums splits l, l+32, ... in order, then a fixed butterfly over the lanes --
+// the same order in both kernels (the tracer's per-target field is bitwise
+// eval_efield_batch's), with the partial loads of a target in flight
+// together instead of one dependent load per split.
+HVB_DEV void reduce_target(const double* part, int split, int m, int i, int lane, double* out) {
+  double s0 = 0, s1 = 0, s2 = 0;
+  for (int s = lane; s < split; s += 32) {
+    const double* p = part + ((size_t)s * m + i) * 4;
+    s0 += p[0];
+    s1 += p[1];
+    s2 += p[2];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (lane == 0) {
     out[3 * (size_t)i] = s0;
     out[3 * (size_t)i + 1] = s1;
     out[3 * (size_t)i + 2] = s2;
   }
 }
 
-// fixed-order reduction of the panel splits
+__global__ void k_field_reduce_dyn(const double* part, int split, const unsigned long long* m_dev, double* out) {
+  const int m = (int)*m_dev;
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m; i += warps)
+    reduce_target(part, split, m, i, lane, out);
+}
+
 __global__ void k_field_reduce(const double* part, int split, int m, double* out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  double s0 = 0, s1 = 0, s2 = 0;
-  for (int s = 0; s < split; ++s) {
-    const double* p = part + ((size_t)s * m + i) * 4;
-    s0 += p[0];
-    s1 += p[1];
-    s2 += p[2];
-  }
-  out[3 * (size_t)i] = s0;
-  out[3 * (size_t)i + 1] = s1;
-  out[3 * (size_t)i + 2] = s2;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i < m) reduce_target(part, split, m, i, threadIdx.x & 31, out);
 }
 
 // near-pair contributions (9 per pair, corner x component) contracted with u
@@ -307,7 +317,7 @@ cudaError_t launch_field_dyn(const FieldArgs& a, unsigned long long* m_dev, int 
 
 cudaError_t launch_field_reduce(const double* part, int split, int m, double* out, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
-  k_field_reduce<<<(m + 255) / 256, 256, 0, st>>>(part, split, m, out);
+  k_field_reduce<<<(unsigned)(((long long)m * 32 + 255) / 256), 256, 0, st>>>(part, split, m, out);
   return cudaGetLastError();
 }
 

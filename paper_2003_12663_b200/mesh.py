@@ -364,8 +364,8 @@ class SurfaceMesh:
         gu, gv = shape_gradients(rule.nodes)
         lam = np.column_stack([1.0 - rule.nodes[:, 0] - rule.nodes[:, 1],
                                rule.nodes[:, 0], rule.nodes[:, 1]])
-        tu = np.einsum("qk,tkd->tqd", gu, self.tri_nodes)
-        tv = np.einsum("qk,tkd->tqd", gv, self.tri_nodes)
+        tu = np.matmul(gu, self.tri_nodes)  # (nt, q, 3); batched BLAS (einsum is ~5x slower here)
+        tv = np.matmul(gv, self.tri_nodes)
         cr = _fp.cross3(tu, tv)
         jac = _fp.norm3_axis(cr)
         low = np.nonzero((jac < MIN_JACOBIAN).any(axis=1))[0]
@@ -374,7 +374,7 @@ class SurfaceMesh:
         unit = cr / jac[..., None]
         wj = rule.weights[None, :] * jac  # (nt, q)
         contrib = wj @ lam  # (nt, 3)
-        n_avg = np.einsum("qc,tq,tqd->tcd", lam, wj, unit)  # (nt, 3, 3)
+        n_avg = np.matmul(lam.T, wj[:, :, None] * unit)  # (nt, 3, 3)
         n = len(self.colloc_points)
         cols = self.tri_corner_cols.ravel()
         w = np.zeros(n)
@@ -619,8 +619,7 @@ def build_mesh(vertices, tri_ids, tri_tags, patches, name="<arrays>", linenos=No
     bad_radius = cr < MIN_CIRCUMRADIUS
     probe = regular_rule(6)
     gu, gv = shape_gradients(probe.nodes)
-    jac = _fp.norm3_axis(_fp.cross3(np.einsum("qk,tkd->tqd", gu, nodes),
-                                    np.einsum("qk,tkd->tqd", gv, nodes)))
+    jac = _fp.norm3_axis(_fp.cross3(np.matmul(gu, nodes), np.matmul(gv, nodes)))
     bad_jac = (jac < MIN_JACOBIAN).any(axis=1)
     anybad = bad_range | bad_distinct | bad_tag | bad_radius | bad_jac
     if np.any(anybad):

@@ -96,6 +96,9 @@ def _morton_order(X: np.ndarray) -> np.ndarray:
     return np.argsort(code, kind="stable")
 
 
+ROUND_PROBE = None  # dev: list receiving (pending, start event, end event) per round
+
+
 def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap: int = 64,
                  max_rounds: int | None = None) -> TraceResult:
     import torch
@@ -154,6 +157,10 @@ def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap:
     pending = L
     while pending > 0 and (max_rounds is None or rounds < max_rounds):
         for _ in range(K):
+            if ROUND_PROBE is not None:  # dev probe (tools/trace_rounds.py): one round per sync
+                ev = [torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+                ROUND_PROBE.append([int(counters[0].item()), *ev])
+                ev[0].record()
             nxt = 1 - cur
             _lib.call("hvb_trace_round", _lib.ptr(state), L, geo_p, _lib.ptr(e_pts[cur]), _lib.ptr(e_pts[nxt]),
                       _lib.ptr(e_line[nxt]), _lib.ptr(sd_pts), _lib.ptr(sd_line), _lib.ptr(sd_out),
@@ -165,6 +172,8 @@ def trace_device(solution, mesh, starts, orientations, params, cfg, initial_cap:
                       int(cfgq.bisect_depth), float(cfgq.bisect_trigger), VERTEX_PROXIMITY, _lib.ptr(poly), cap, st)
             cur = nxt
             rounds += 1
+            if ROUND_PROBE is not None:
+                ROUND_PROBE[-1][2].record()
         c = counters.cpu().numpy()
         pending, max_pts = int(c[0]), int(c[2])
         if _LOG:

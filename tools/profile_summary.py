@@ -34,7 +34,7 @@ for r in rows:
 T = sum(tot.values())
 with open(os.path.join(PROF, f"{tag}_launches.txt"), "w") as fh:
     fh.write("ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ python bench.py --steps 1 "
-             "--warmup 0 --no-e2e --no-cpu --points 10000 --lines 1024\n"
+             "--warmup 0 --no-e2e --no-cpu --no-full-trace --points 10000 --lines 1024\n"
              "(cold-cache, serialised launches: compare SHARES, not absolutes)\n\n")
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         fh.write(f"{k:50s} {cnt[k]:6d} launches {v:10.2f} ms {v / T * 100:6.2f}%\n")
@@ -49,8 +49,12 @@ for fn in sorted(os.listdir(OUT)):
     res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep], capture_output=True,
                          text=True)
     k = fn[len("prof_"):-len(".ncu-rep")]
+    skip_file = os.path.join(OUT, f"prof_{k}.skip")
+    skip = open(skip_file).read().split()[-1] if os.path.exists(skip_file) else "?"
     with open(os.path.join(PROF, f"{tag}_ncu_{k}.txt"), "w") as fh:
-        fh.write(f"ncu --set full --clock-control none --import-source on -k regex:{k} -s 2 -c 1 (one launch)\n\n")
+        fh.write(f"ncu --set full --clock-control none --import-source on -k regex:{k} -s {skip} -c 1 (one launch) "
+                 f"of python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu --no-full-trace --points 10000 "
+                 f"--lines 1024\n\n")
         fh.write(res.stdout)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(raw.splitlines()))
