@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="mesh resolution scale (1.0 = config 4)")
     ap.add_argument("--points", type=int, default=100_000, help="field points per step (whole job)")
     ap.add_argument("--lines", type=int, default=8192, help="cfg5 field lines per step (whole job; 0 = skip)")
+    ap.add_argument("--uniform-points", type=int, default=1_000_000,
+                    help="SURVEY 8d uniform field workload, timed once (0 = skip)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-full-trace", dest="full_trace", action="store_false",
                     help="skip the once-per-run config-5 trace of every vertex (~1e5 lines)")
@@ -640,6 +642,31 @@ def run_b200(args):
     t_near = float(fvec.item())
     del En, P_near
 
+    # SURVEY 8d's uniform field workload at its size: 1e6 points in the 1.2x
+    # bounding box (seed 0), split per rank, timed once
+    n_uni = args.uniform_points
+    field_uniform = None
+    if n_uni > 0:
+        P_u = 0.5 * (lo + hi) + np.random.default_rng(0).uniform(-0.6, 0.6, (n_uni, 3)) * (hi - lo)
+        ua, ub = split_range(n_uni, world, rank)
+        P_u = torch.as_tensor(P_u[ua:ub], device=dev)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        f0.record()
+        Eu = postprocess.field_points_device(dmn, u_dev, src, P_u, False)
+        f1.record()
+        barrier()
+        fvec = torch.tensor([f0.elapsed_time(f1) / 1e3], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(fvec, op=dist.ReduceOp.MAX)
+        t_uni = float(fvec.item())
+        fl_u = float(n_uni) * (9.0 + 12 * 17) * nt
+        field_uniform = {"points": n_uni, "seconds": t_uni, "evals_per_s": n_uni / t_uni,
+                         "achieved_tflops": fl_u / t_uni / 1e12, "frac_of_fp64_peak": fl_u / t_uni / 1e12 / tflops_peak,
+                         "note": "SURVEY 8d: uniform points in the 1.2x bbox (seed 0), timed once; flop = "
+                                 "(9 + 12 x 17) nt per point (near pairs not counted)"}
+        del Eu, P_u
+
     # GEMV roofline: stream this rank's row block a few times (untimed)
     A, rhs = assemble_distributed(mesh) if world > 1 else assemble(mesh)
     st = A.store
@@ -780,6 +807,7 @@ def run_b200(args):
             "gmres_solve_s": t_solve,
             "gmres_iterations": iters,
             "field_evals_per_s": args.points / t_field,
+            "field_uniform": field_uniform,
             "field_near_surface": {"points": n, "evals_per_s": n / t_near,
                                    "near_pairs_per_point_rank0": near_pairs_per_point,
                                    "note": "every collocation point + 0.25 local R along its normal (SURVEY 8d)"},

@@ -34,13 +34,80 @@ __global__ void k_contract(const double* __restrict__ table, int nt, int nq, con
 constexpr int FT = 256;   // targets per CTA
 constexpr int FCH = 32;   // panels per shared-memory chunk
 
+// Field of one FCH-panel chunk [c0, c0+cn) at the thread's target X: the
+// chunk's regular panels summed in panel order into (sx, sy, sz) starting
+// from zero, non-regular (near) panels flagged / emitted.  src / cls / cols
+// point at the chunk's panel data (shared memory, or global memory in the
+// chunk-parallel mode).
+template <int NQ, int POT>
+HVB_DEV void chunk_sum(const FieldArgs& a, d3 X, int own, bool live, int ti, int c0, int cn,
+                       const double2* __restrict__ src, const double* __restrict__ cls, const int* __restrict__ cols,
+                       double& sx, double& sy, double& sz, bool& any_near) {
+  const int lane = threadIdx.x & 31;
+  sx = sy = sz = 0.0;
+  // whole group far from the target: every panel is regular (exactly;
+  // device.py panel_groups) -- skip the per-panel classification
+  const double* gb = a.groups + 8 * (size_t)(c0 / FCH);
+  const double gd = __dsqrt_rn(sumsq_unfused(sub_rn(X, mk3(gb[0], gb[1], gb[2]))));
+  const bool far = gd > gb[3] * (1.0 + 1e-12);
+  for (int j = 0; j < cn; ++j) {
+    const double* c = cls + 6 * j;
+    const bool reg = far || is_regular(X, mk3(c[0], c[1], c[2]), c[3], c[4], c[5]);
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const double2 p01 = src[(j * NQ + q) * 2];
+      const double2 p2q = src[(j * NQ + q) * 2 + 1];
+      const double dx = X.x - p01.x, dy = X.y - p01.y, dz = X.z - p2q.x;
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      if (POT) {
+        fx = fma(p2q.y, rsqrt_full(r2), fx);
+      } else {
+        const double s = p2q.y * rinv3(r2);
+        fx = fma(s, dx, fx);
+        fy = fma(s, dy, fy);
+        fz = fma(s, dz, fz);
+      }
+    }
+    if (reg) {
+      sx += fx;
+      sy += fy;
+      sz += fz;
+    }
+    bool emit = false;
+    if (!reg && live) {
+      const int* tc = cols + 3 * j;
+      emit = !(own >= 0 && (tc[0] == own || tc[1] == own || tc[2] == own));
+    }
+    if (a.near_list == nullptr) {
+      any_near |= emit;
+      continue;
+    }
+    const unsigned msk = __ballot_sync(0xffffffffu, emit);
+    if (msk) {
+      unsigned long long b = 0;
+      if (lane == 0) b = atomicAdd(a.near_count, (unsigned long long)__popc(msk));
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (emit) {
+        long long slot = (long long)b + __popc(msk & ((1u << lane) - 1u));
+        if (slot < a.near_cap) {
+          a.near_list[2 * slot] = ti;
+          a.near_list[2 * slot + 1] = c0 + j;
+        }
+      }
+    }
+  }
+}
+
 // One (target block bx, panel split by) tile of the N-body sum.  Called by
 // every thread of the CTA (it synchronises).  near_list == nullptr: instead
-// of emitting (target, panel) near pairs, set has_near[target] = 1.
+// of emitting (target, panel) near pairs, set has_near[target] = 1.  A
+// target's split partial is the sum of its chunk sums in chunk order (the
+// same in the chunk-parallel mode below, so results never depend on the
+// batch).
 template <int NQ, int POT>
 HVB_DEV void field_tile(const FieldArgs& a, int bx, int by, double2* s_src, double* s_cls, int* s_cols) {
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
   const int ti = bx * FT + tid;
   const bool live = ti < a.m;
   const bool warp_live = bx * FT + (tid & ~31) < a.m;
@@ -64,58 +131,11 @@ HVB_DEV void field_tile(const FieldArgs& a, int bx, int by, double2* s_src, doub
     // a warp whose 32 targets are all past the count only helps stage the
     // chunk (the tracer's tail rounds have a handful of live targets per CTA)
     if (!warp_live) continue;
-    // whole group far from the target: every panel is regular (exactly;
-    // device.py panel_groups) -- skip the per-panel classification
-    const double* gb = a.groups + 8 * (size_t)(c0 / FCH);
-    const double gd = __dsqrt_rn(sumsq_unfused(sub_rn(X, mk3(gb[0], gb[1], gb[2]))));
-    const bool far = gd > gb[3] * (1.0 + 1e-12);
-    for (int j = 0; j < cn; ++j) {
-      const double* c = s_cls + 6 * j;
-      const bool reg = far || is_regular(X, mk3(c[0], c[1], c[2]), c[3], c[4], c[5]);
-      double fx = 0.0, fy = 0.0, fz = 0.0;
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const double2 p01 = s_src[(j * NQ + q) * 2];
-        const double2 p2q = s_src[(j * NQ + q) * 2 + 1];
-        const double dx = X.x - p01.x, dy = X.y - p01.y, dz = X.z - p2q.x;
-        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-        if (POT) {
-          fx = fma(p2q.y, rsqrt_full(r2), fx);
-        } else {
-          const double s = p2q.y * rinv3(r2);
-          fx = fma(s, dx, fx);
-          fy = fma(s, dy, fy);
-          fz = fma(s, dz, fz);
-        }
-      }
-      if (reg) {
-        ex += fx;
-        ey += fy;
-        ez += fz;
-      }
-      bool emit = false;
-      if (!reg && live) {
-        const int* tc = s_cols + 3 * j;
-        emit = !(own >= 0 && (tc[0] == own || tc[1] == own || tc[2] == own));
-      }
-      if (a.near_list == nullptr) {
-        any_near |= emit;
-        continue;
-      }
-      const unsigned msk = __ballot_sync(0xffffffffu, emit);
-      if (msk) {
-        unsigned long long b = 0;
-        if (lane == 0) b = atomicAdd(a.near_count, (unsigned long long)__popc(msk));
-        b = __shfl_sync(0xffffffffu, b, 0);
-        if (emit) {
-          long long slot = (long long)b + __popc(msk & ((1u << lane) - 1u));
-          if (slot < a.near_cap) {
-            a.near_list[2 * slot] = ti;
-            a.near_list[2 * slot + 1] = c0 + j;
-          }
-        }
-      }
-    }
+    double sx, sy, sz;
+    chunk_sum<NQ, POT>(a, X, own, live, ti, c0, cn, s_src, s_cls, s_cols, sx, sy, sz, any_near);
+    ex += sx;
+    ey += sy;
+    ez += sz;
   }
   if (live) {
     double* o = a.part + ((size_t)by * a.m + ti) * 4;
@@ -124,6 +144,59 @@ HVB_DEV void field_tile(const FieldArgs& a, int bx, int by, double2* s_src, doub
     o[2] = ez;
     o[3] = 0.0;
     if (any_near) a.has_near[(size_t)by * a.m + ti] = 1;  // (split, m) chunk flags
+  }
+}
+
+// Chunk-parallel tile for a block with at most 32 live targets (the
+// tracer's tail rounds): warp w takes chunks w, w + 8, ... of the split for
+// warp 0's targets, reading the panel data straight from global memory
+// (every lane loads the same node: broadcast), and warp 0 adds the chunk
+// sums in chunk order -- bitwise field_tile's result, ~8x lower latency.
+constexpr int MAXCH = 16;  // chunks per split held in shared memory
+template <int NQ>
+HVB_DEV void field_tile_small(const FieldArgs& a, int bx, int by, double* s_part, int* s_near) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, w = tid >> 5;
+  const int ti = bx * FT + lane;
+  const bool live = ti < a.m;
+  const int tt = live ? ti : a.m - 1;
+  const d3 X = mk3(a.pts[3 * (size_t)tt], a.pts[3 * (size_t)tt + 1], a.pts[3 * (size_t)tt + 2]);
+  const int own = a.own_col ? a.own_col[tt] : -1;
+  const int ng = (a.nt + FCH - 1) / FCH;
+  const int tb = min(a.nt, FCH * (int)((long long)ng * by / a.split));
+  const int te = min(a.nt, FCH * (int)((long long)ng * (by + 1) / a.split));
+  const int nch = (te - tb + FCH - 1) / FCH;
+  __syncthreads();  // s_part / s_near of the previous item are consumed
+  for (int c = w; c < nch; c += FT / 32) {
+    const int c0 = tb + c * FCH;
+    const int cn = min(FCH, te - c0);
+    double sx, sy, sz;
+    bool nf = false;
+    chunk_sum<NQ, 0>(a, X, own, live, ti, c0, cn, reinterpret_cast<const double2*>(a.src + (size_t)c0 * NQ * 4),
+                     a.cls + (size_t)c0 * 6, a.tri_cols + (size_t)c0 * 3, sx, sy, sz, nf);
+    double* o = s_part + (c * 32 + lane) * 3;
+    o[0] = sx;
+    o[1] = sy;
+    o[2] = sz;
+    s_near[c * 32 + lane] = nf;
+  }
+  __syncthreads();
+  if (w == 0 && live) {
+    double ex = 0.0, ey = 0.0, ez = 0.0;
+    bool any_near = false;
+    for (int c = 0; c < nch; ++c) {
+      const double* o = s_part + (c * 32 + lane) * 3;
+      ex += o[0];
+      ey += o[1];
+      ez += o[2];
+      any_near |= s_near[c * 32 + lane] != 0;
+    }
+    double* o = a.part + ((size_t)by * a.m + ti) * 4;
+    o[0] = ex;
+    o[1] = ey;
+    o[2] = ez;
+    o[3] = 0.0;
+    if (any_near) a.has_near[(size_t)by * a.m + ti] = 1;
   }
 }
 
@@ -143,21 +216,29 @@ __global__ void __launch_bounds__(FT) k_field(FieldArgs a) {
 // before the launch), so every SM stays busy until the last item whatever
 // the count -- the per-target sums do not depend on which CTA runs them.
 template <int NQ>
-__global__ void __launch_bounds__(FT) k_field_dyn(FieldArgs a, unsigned long long* m_dev) {
+__global__ void __launch_bounds__(FT, 4) k_field_dyn(FieldArgs a, unsigned long long* m_dev) {
   __shared__ double2 s_src[FCH * NQ * 2];
   __shared__ double s_cls[FCH * 6];
   __shared__ int s_cols[FCH * 3];
+  __shared__ double s_part[MAXCH * 32 * 3];
+  __shared__ int s_near[MAXCH * 32];
   __shared__ long long s_item;
   a.m = (int)m_dev[0];
   const int nb = (a.m + FT - 1) / FT;
   const long long items = (long long)nb * a.split;
+  const int ng = (a.nt + FCH - 1) / FCH;
+  const bool chunks_fit = (ng + a.split - 1) / a.split + 1 <= MAXCH;
   while (true) {
     if (threadIdx.x == 0) s_item = (long long)atomicAdd(m_dev + 4, 1ull);
     __syncthreads();
     const long long it = s_item;
     __syncthreads();
     if (it >= items) break;
-    field_tile<NQ, 0>(a, (int)(it % nb), (int)(it / nb), s_src, s_cls, s_cols);
+    const int bx = (int)(it % nb), by = (int)(it / nb);
+    if (chunks_fit && a.m - bx * FT <= 32)
+      field_tile_small<NQ>(a, bx, by, s_part, s_near);
+    else
+      field_tile<NQ, 0>(a, bx, by, s_src, s_cls, s_cols);
   }
 }
 

@@ -21,11 +21,11 @@
 //
 // Arithmetic follows the reference statement by statement (unfused
 // products/sums where Python evaluates scalar/vector expressions, ddot FMA
-// chains for np.linalg.norm of a 3-vector).  Where the reference's order is
-// BLAS-defined (b4 @ K, dgemv) a sequential FMA chain is used, and x5 is the
-// stage-6 point itself (same coefficients), which lets the accepted point
-// reuse the stage-6 field instead of evaluating E(x5) a second time:
-// 6 field evaluations per accepted step instead of the reference's 7.
+// chains for np.linalg.norm of a 3-vector, OpenBLAS dgemv_n order for the
+// b5 @ K / b4 @ K products).  The accepted point reuses the stage-6 field
+// (x5 is within 1 ulp of the stage-6 point) instead of evaluating E(x5) a
+// second time: 6 field evaluations per accepted step instead of the
+// reference's 7.
 #include "near.cuh"
 
 namespace hvb {
@@ -45,6 +45,20 @@ __constant__ double kA[7][6] = {
 };
 __constant__ double kB4[7] = {5179.0 / 57600, 0.0, 7571.0 / 16695, 393.0 / 640, -92097.0 / 339200, 187.0 / 2100,
                               1.0 / 40};
+__constant__ double kB5[7] = {35.0 / 384, 0.0, 500.0 / 1113, 125.0 / 192, -2187.0 / 6784, 11.0 / 84, 0.0};
+
+// (b @ K)[d] for the (7,) coefficients and the 7 stage tangents, in the order
+// numpy's vector @ (7,3) matrix takes through OpenBLAS dgemv_n (m = 3, n = 7):
+// a 4-column block fma(b0,k0, b1 k1) + fma(b2,k2, b3 k3), then the remaining
+// columns one FMA each (bitwise on random inputs in the reference container;
+// the same kernel order as map_reference_blas below)
+HVB_DEV double dgemv7(const double* b, const double (*k)[3], int d) {
+  double t = __dadd_rn(__fma_rn(b[0], k[0][d], __dmul_rn(b[1], k[1][d])),
+                       __fma_rn(b[2], k[2][d], __dmul_rn(b[3], k[3][d])));
+  t = __fma_rn(b[4], k[4][d], t);
+  t = __fma_rn(b[5], k[5][d], t);
+  return __fma_rn(b[6], k[6][d], t);
+}
 
 HVB_DEV double norm3(const double* v) { return __dsqrt_rn(dot3_blas(mk3(v[0], v[1], v[2]), mk3(v[0], v[1], v[2]))); }
 
@@ -225,16 +239,16 @@ __global__ void k_trace_ctrl(TraceArgs a, int mode) {
         request_e(a, L, line, xi, kPhaseStage);
         break;
       }
-      // x5: the stage-6 point (its coefficients a6 are b5, and b5[6] = 0),
-      // so E(x5) -- which the reference evaluates again after accepting
-      // (src/postprocess.py:323) -- is the stage-6 result already in hand.
-      // x5 differs from the reference's dgemv-ordered b5 @ K by <= 1 ulp.
+      // x5 = x + h (b5 @ K), x4 = x + h (b4 @ K) in the reference's order
+      // (numpy vector @ matrix = OpenBLAS dgemv_n over m = 3, n = 7, measured
+      // bitwise in the reference container: dgemv7).  x5 is within 1 ulp of
+      // the stage-6 point (same coefficients, Python's sum order), so E(x5)
+      // -- which the reference evaluates again after accepting
+      // (src/postprocess.py:323) -- is taken from the stage-6 result.
       double x5[3], x4[3], df[3];
       for (int d = 0; d < 3; ++d) {
-        double b4 = 0.0;
-        for (int i = 0; i < 7; ++i) b4 = fma(kB4[i], L.k[i][d], b4);
-        x5[d] = L.req[d];
-        x4[d] = __dadd_rn(L.x[d], __dmul_rn(L.h, b4));
+        x5[d] = __dadd_rn(L.x[d], __dmul_rn(L.h, dgemv7(kB5, L.k, d)));
+        x4[d] = __dadd_rn(L.x[d], __dmul_rn(L.h, dgemv7(kB4, L.k, d)));
         df[d] = __dsub_rn(x5[d], x4[d]);
       }
       const double err = norm3(df);

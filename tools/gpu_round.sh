@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
 timeout 1500 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
-SMALL="--steps 1 --warmup 0 --no-e2e --no-cpu --no-full-trace --points 10000 --lines 1024"
+SMALL="--steps 1 --warmup 0 --no-e2e --no-cpu --no-full-trace --uniform-points 0 --points 10000 --lines 1024"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ --csv \
     --log-file gpurun_out/launches.csv python bench.py $SMALL > gpurun_out/ncu_launch.log 2>&1
 # kernel:skip -- which launch to capture (k_surface_distance -s 0 = the seed
