@@ -58,20 +58,32 @@ int hvb_sweep_geometry(int* out);
 /* Column tiling of the regular sweep (HOST function, host pointers; no
  * GPU needed; csrc/tiling.cpp): recursive coordinate bisection of the n
  * collocation points into tiles of <= max_tile columns swept along their
- * longest axis, one record per (panel, tile owning one of its corners)
- * sorted by first owned column, grouped in stages of `group` records with
- * disjoint owned corners within `band` columns (short stages padded with
- * dummy records, panel -1).  sizes = (n_tiles, n_records, band, real
- * records); fetch copies perm (n), tile_col0/width (n_tiles), tile_ptr
+ * longest axis (the tile's owned columns), one record per panel in the
+ * lowest-numbered tile owning one of its corners; a tile's local columns
+ * are its owned columns plus its halo (its panels' corners owned by later
+ * tiles), numbered along the sweep axis; records sorted by first local
+ * column, grouped in stages of `group` records with disjoint corners within
+ * `band` columns (short stages padded with dummy records, panel -1).
+ * sizes = (n_tiles, n_records, band, real records, local columns,
+ * exchange entries, slots, halo copies, producer entries = consumer
+ * entries); fetch copies
+ * perm (n), tile_col0/width (n_tiles: owned device columns), tile_ptr
  * (n_tiles + 1), ent_tri (n_records), ent_meta (n_records x 5: mfirst, l0,
- * l1, l2, flags) and free releases the handle.  Returns 0, 1 (bad
+ * l1, l2, flags; l = local column), tile_lptr (n_tiles + 1), lcol (local
+ * columns: device column, or ~slot of a halo copy / receiving column's
+ * partial), tile_xptr (n_tiles + 1), xent (entries x 4: slot, device
+ * column, first, last -- per receiving column its partial, then its halo
+ * copies by producer), tile_pptr (n_tiles + 1) / prods (distinct
+ * producer tiles per tile) and tile_cptr (n_tiles + 1) / cons (distinct
+ * consumer tiles per tile); free releases the handle.  Returns 0, 1 (bad
  * argument) or 2 (band not bounded).
  * Replaces: nothing in the reference (its rows are independent NumPy
  * sweeps, assembly.py:173-200); this is the schedule of hvb_assemble_regular. */
 int hvb_tiling_build(const double* points, int n, const int* tri_cols, int nt, int max_tile, int band, int group,
                      long long* sizes, void** handle);
 int hvb_tiling_fetch(void* handle, int* perm, int* tile_col0, int* tile_width, long long* tile_ptr, int* ent_tri,
-                     int* ent_meta);
+                     int* ent_meta, int* tile_lptr, int* lcol, int* tile_xptr, int* xent, int* tile_pptr,
+                     int* prods, int* tile_cptr, int* cons);
 int hvb_tiling_free(void* handle);
 
 /* Per-panel device arrays from the flat circumcircles (cc (nt,3), R (nt)):
@@ -90,14 +102,27 @@ int hvb_panel_data(const double* circumcenters, const double* radii, int nt, dou
  * each entry written once as row_scale * sum, for row-list entries
  * [row_begin, row_begin+n_rows).  hats (HOST pointer) = nq x 3 hat values
  * hat_c(q) of the regular rule.  Non-regular, non-singular pairs are
- * appended to near_list as (row-list index, triangle).
+ * appended to near_list as (row-list index, triangle).  Schedule arrays
+ * from hvb_tiling_fetch (device copies; xent as int4).  A column local to
+ * several tiles is summed in a fixed order: every tile leaves its raw sums
+ * of such a column in a slot of `halo`; whichever CTA (same rows) is the
+ * last of the owner and its producers to finish adds the owner's partial
+ * and the copies in producer order and writes the entry (completion
+ * counters in `sched`; no CTA waits on another).
  * Replaces: row_pass1 regular part  assembly.py:170-200 and
  * _kernel_values 126-132 */
-int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_col0,
-                         const int* tile_width, int n_tiles, int nq, const double* hats, int row_begin, int n_rows,
-                         const double* rowdata, const int* row_col, const double* row_scale,
-                         const long long* row_out, double* A, long long part_ld, const int* tri_cols, int mode,
-                         int* near_list, unsigned long long* near_count, long long near_cap, void* stream);
+int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_lptr,
+                         const int* lcol, const int* tile_xptr, const int* xent, const int* tile_pptr,
+                         const int* prods, const int* tile_cptr, const int* cons, int n_tiles, int nq,
+                         const double* hats, int row_begin, int n_rows, const double* rowdata, const int* row_col,
+                         const double* row_scale, const long long* row_out, double* A, long long part_ld,
+                         const int* tri_cols, int mode, double* halo, int* sched, int* near_list,
+                         unsigned long long* near_count, long long near_cap, void* stream);
+/* Device scratch of one hvb_assemble_regular call: `sched` holds
+ * hvb_sweep_sched_ints(n_rows, n_tiles) ints (zeroed by the call: one
+ * completion counter per (row block, tile)); `halo` holds
+ * n_slots x n_rows doubles (exchange slots, csrc/tiling.cpp). */
+long long hvb_sweep_sched_ints(int n_rows, int n_tiles);
 
 /* K4 (+K6 diagonal) -- singular corner pairs with the split-corner Duffy
  * rule (3 x n_rule x 4 table), then A[row, own] += row_diag.

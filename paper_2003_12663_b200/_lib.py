@@ -26,7 +26,7 @@ SIGNATURES = {
     "hvb_build_stream": [_P, _I, _P, _D, _P, _P, _LL, _I, _I, _P, _P],
     "hvb_panel_data": [_P, _P, _I, _D, _P, _P, _P, _P],
     "hvb_sweep_geometry": [_P],
-    "hvb_assemble_regular": [_P, _P, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _LL, _P, _I, _P, _P, _LL, _P],
+    "hvb_assemble_regular": [_P] * 10 + [_I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _LL, _P, _I, _P, _P, _P, _P, _LL, _P],
     "hvb_assemble_singular": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P],
     "hvb_charge_reduce": [_P, _I, _LL, _I, _P, _I, _P],
     "hvb_fill_float_cols": [_P, _P, _P, _I, _I, _I, _P],
@@ -56,7 +56,7 @@ SIGNATURES = {
     "hvb_near_coincide": [_P, _LL, _P, _P, _D, _P, _P],
     "hvb_streamer": [_P, _P, _I, _I, _P, _P, _I, _D, _P, _P, _P],
     "hvb_tiling_build": [_P, _I, _P, _I, _I, _I, _I, _P, _P],
-    "hvb_tiling_fetch": [_P, _P, _P, _P, _P, _P, _P],
+    "hvb_tiling_fetch": [_P] * 15,
     "hvb_tiling_free": [_P],
     "hvb_bench_dfma": [_P, _I, _I, _P],
     "hvb_bench_read": [_P, _LL, _P, _I, _P],
@@ -104,6 +104,8 @@ def lib():
             h.hvb_ipc_handle_bytes.argtypes = []
             h.hvb_stream_record_doubles.restype = _I
             h.hvb_stream_record_doubles.argtypes = [_I, _I]
+            h.hvb_sweep_sched_ints.restype = _LL
+            h.hvb_sweep_sched_ints.argtypes = [_I, _I]
             _lib = h
     return _lib
 

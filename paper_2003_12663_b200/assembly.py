@@ -57,6 +57,7 @@ KERNEL_SL = "sl"
 KERNEL_ADL = "adl"
 KERNEL_E = "efield"
 LDA_ALIGN = 32  # row pitch in elements (256-byte aligned rows for the GEMV)
+HALO_BYTES = 40 << 30  # scratch cap of one regular-sweep launch (exchange slots; also <= 1/3 of free memory)
 # precision="single" matrices: False (default) reduces every row in float32
 # as the reference's float32 dot does; True keeps float32 products but sums
 # in double (more accurate, not the reference's arithmetic)
@@ -398,12 +399,24 @@ def _run_rows_on(dm, plan: RowPlan, A, counts: dict, part_ld: int = 0):
         near = torch.empty((cap, 2), dtype=torch.int32, device=dev)
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
         for lo, hi, mode in ((0, plan.n_sl, 0), (plan.n_sl, plan.m, 1)):
-            if hi > lo:
+            # launches of <= HALO_BYTES of exchange slots (csrc/tiling.cpp 5):
+            # one launch per row kind when memory allows (each launch has a tail)
+            have = getattr(dm, "_slots", None)
+            cap = max(0 if have is None else have.numel() * 8,
+                      min(HALO_BYTES, torch.cuda.mem_get_info(dev)[0] // 3))
+            step = max(128, cap // (8 * max(1, dm.n_slots)) // 128 * 128)
+            for a in range(lo, hi, step):
+                b = min(hi, a + step)
+                halo = dm.sweep_slots(dm.n_slots * (b - a))
+                sched = torch.empty(int(_lib.lib().hvb_sweep_sched_ints(b - a, dm.n_tiles)), dtype=torch.int32,
+                                    device=dev)
                 _lib.call(
                     "hvb_assemble_regular", _lib.ptr(dm.stream_for(mode)), _lib.ptr(dm.tile_ptr),
-                    _lib.ptr(dm.tile_col0), _lib.ptr(dm.tile_width), dm.n_tiles, dm.nq, hats, lo, hi - lo,
-                    _lib.ptr(plan.rowdata), _lib.ptr(plan.col), _lib.ptr(plan.scale), _lib.ptr(plan.out),
-                    _lib.ptr(A), part_ld, _lib.ptr(dm.tri_cols), mode, _lib.ptr(near), _lib.ptr(cnt), cap, s)
+                    _lib.ptr(dm.tile_lptr), _lib.ptr(dm.lcol), _lib.ptr(dm.tile_xptr), _lib.ptr(dm.xent),
+                    _lib.ptr(dm.tile_pptr), _lib.ptr(dm.prods), _lib.ptr(dm.tile_cptr), _lib.ptr(dm.cons),
+                    dm.n_tiles, dm.nq, hats, a, b - a, _lib.ptr(plan.rowdata), _lib.ptr(plan.col),
+                    _lib.ptr(plan.scale), _lib.ptr(plan.out), _lib.ptr(A), part_ld, _lib.ptr(dm.tri_cols), mode,
+                    _lib.ptr(halo), _lib.ptr(sched), _lib.ptr(near), _lib.ptr(cnt), cap, s)
         n_near = int(cnt.item())
         if n_near <= cap:
             break

@@ -36,6 +36,9 @@
 #ifndef HVB_SWEEP_WIN
 #define HVB_SWEEP_WIN 64
 #endif
+#ifndef HVB_SWEEP_FLUSH
+#define HVB_SWEEP_FLUSH 16
+#endif
 #ifndef HVB_SWEEP_WPC
 #define HVB_SWEEP_WPC 4
 #endif
@@ -50,7 +53,7 @@ constexpr int STRIDE = 33;
 constexpr int WIN = HVB_SWEEP_WIN;                       // window columns
 constexpr int SLOTS = WIN + 1;                           // + dump slot
 constexpr int WREG = (SLOTS * STRIDE + 1) & ~1;          // doubles per warp window (16-byte aligned)
-constexpr int FLUSH = 16;                                // columns per flush (band <= WIN - FLUSH)
+constexpr int FLUSH = HVB_SWEEP_FLUSH;                   // columns per flush (band <= WIN - FLUSH)
 constexpr int R = 4;                                     // records per stage
 constexpr int WPC = HVB_SWEEP_WPC;                       // warps per CTA
 constexpr int MINB = HVB_SWEEP_MINB;                     // resident CTAs per SM (register budget)
@@ -122,11 +125,20 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
   const int wib = threadIdx.x >> 5;
   double* win = ring + S * R * REC + wib * WREG;
 
-  const int cta_row0 = blockIdx.x * (WPC * ROWS);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, 1);
+      released[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nrb = gridDim.x;
+  const int rb = blockIdx.x, tile = blockIdx.y;
+  const int cta_row0 = rb * (WPC * ROWS);
   const int live_warps = min(WPC, (a.n_rows - cta_row0 + ROWS - 1) / ROWS);
-  const int tile = blockIdx.y;
   const int64_t e0 = a.tile_ptr[tile], e1 = a.tile_ptr[tile + 1];
-  const int col0 = a.tile_col0[tile], width = a.tile_width[tile];
+  const int lp0 = a.tile_lptr[tile], width = a.tile_lptr[tile + 1] - lp0;
   const double* src = a.stream + e0 * REC;
   const int ne = (int)(e1 - e0);
   const int ns = (ne + R - 1) / R;
@@ -136,14 +148,6 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     bulk_load(ring + (p % S) * (R * REC), src + (size_t)(R * p) * REC, (unsigned)(nrec * REC * 8), full + p % S);
   };
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, 1);
-      released[s] = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
   if (threadIdx.x == 0)
     for (int p = 0; p < min(S, ns); ++p) issue(p);
   if (wib >= live_warps) return;  // no live rows: this warp takes no part in the ring
@@ -159,35 +163,49 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
   const int64_t fout = live0 ? (RED ? 0 : a.row_out[lr0]) : -1;
   const double fscale = live0 ? a.row_scale[lr0] * (MODE == 0 ? 0.5 : 1.0) : 0.0;  // SL sums hold 2w/r
   double* const part = RED ? a.A + (int64_t)((a.row_begin + base_row) / ROWS) * a.part_ld : nullptr;
+  double* const halo = a.halo + base_row;  // + slot * n_rows + row
 
   for (int k = lane; k < SLOTS * STRIDE; k += 32) win[k] = 0.0;
 
   int base = 0;
-  // flush 16 finished columns: lanes 0-15 write rows 0-15 and lanes 16-31
-  // rows 16-31 of 16 consecutive columns (128-byte row segments), so the
-  // window only needs band + 16 columns (48 columns hold the band-32 tiling)
+  // flush FLUSH finished columns: lane l writes rows (l / FLUSH) * FLUSH ..
+  // + FLUSH - 1 of local column b + l % FLUSH -- an owned column to its
+  // device column of A (row segments of consecutive device columns), a
+  // halo copy or a receiving column's partial raw to its slot.  The window
+  // only needs band + FLUSH columns.
   auto flush = [&](int b) {
-    const int c = b + (lane & 15);
+    const int c = b + (lane & (FLUSH - 1));
     double* wcol = win + (c % WIN) * STRIDE;
     const bool in = c < width;
-    const int rh = (lane >> 4) * 16;
+    const int dst = in ? a.lcol[lp0 + c] : 0;
+    double* const hcol = halo + (size_t)(dst < 0 ? ~dst : 0) * a.n_rows;
+    const int rh = (lane / FLUSH) * FLUSH;  // FLUSH rows per lane
     if (RED) {
-      double sum = 0.0;  // rows rh .. rh+15 in order, then the two halves
+      double sum = 0.0;  // rows rh .. rh+FLUSH-1 in order, then the row groups
 #pragma unroll 8
-      for (int j = 0; j < 16; ++j) {
+      for (int j = 0; j < FLUSH; ++j) {
         const int row = rh + j;
-        sum = fma(wcol[row], __shfl_sync(0xffffffffu, fscale, row), sum);
+        const double v = wcol[row];
+        const int64_t off = __shfl_sync(0xffffffffu, fout, row);  // every lane: the mask is the full warp
+        sum = fma(v, __shfl_sync(0xffffffffu, fscale, row), sum);
+        if (dst < 0 && in && off >= 0) hcol[row] = v;
         wcol[row] = 0.0;
       }
-      sum += __shfl_xor_sync(0xffffffffu, sum, 16);
-      if (lane < 16 && in) part[col0 + c] = sum;
+#pragma unroll
+      for (int o = FLUSH; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane < FLUSH && in && dst >= 0) part[dst] = sum;
     } else {
 #pragma unroll 8
-      for (int j = 0; j < 16; ++j) {
+      for (int j = 0; j < FLUSH; ++j) {
         const int row = rh + j;
         const int64_t off = __shfl_sync(0xffffffffu, fout, row);
         const double sc = __shfl_sync(0xffffffffu, fscale, row);
-        if (off >= 0 && in) a.A[off + col0 + c] = wcol[row] * sc;
+        if (off >= 0 && in) {
+          if (dst >= 0)
+            a.A[off + dst] = wcol[row] * sc;
+          else
+            hcol[row] = wcol[row];
+        }
         wcol[row] = 0.0;
       }
     }
@@ -358,6 +376,82 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
     flush(base);
     base += FLUSH;
   }
+  // completion: every lane fences its own slot writes, the live warps meet
+  // and warp 0 counts this CTA in for its own tile and for every tile
+  // importing its halo copies.  The CTA that completes a tile's count (its
+  // partials and all copies of its receiving columns written, same rows)
+  // performs that tile's exchange -- nobody waits.
+  __shared__ int s_todo[64];
+  __shared__ int s_ntodo;
+  __threadfence();
+  asm volatile("bar.sync 1, %0;" ::"r"(live_warps * 32) : "memory");
+  if (wib == 0) {
+    const int cb = a.tile_cptr[tile], nc = a.tile_cptr[tile + 1] - cb;
+    int nt = 0;
+    for (int i0 = 0; i0 <= nc; i0 += 32) {
+      const int i = i0 + lane;
+      bool done = false;
+      int t = 0;
+      if (i <= nc) {
+        t = i == 0 ? tile : a.cons[cb + i - 1];
+        const int need = 1 + a.tile_pptr[t + 1] - a.tile_pptr[t];
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.sched + t * nrb + rb) : "memory");
+        done = old == need - 1;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, done);
+      if (done) s_todo[min(63, nt + __popc(m & ((1u << lane) - 1u)))] = t;
+      nt += __popc(m);
+    }
+    __threadfence();
+    if (lane == 0) s_ntodo = min(nt, 64);
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(live_warps * 32) : "memory");
+
+  // exchange of tile t: every receiving column = its partial + the halo
+  // copies of earlier tiles (producer order), scaled and written once;
+  // lane = row, 32 slots loaded per round trip
+  const int ntodo = s_ntodo;
+  for (int k = 0; k < ntodo; ++k) {
+    const int t = s_todo[k];
+    const int xb = a.tile_xptr[t], xe = a.tile_xptr[t + 1];
+    double acc = 0.0;
+    for (int x0 = xb; x0 < xe; x0 += 32) {
+      const int nb = min(32, xe - x0);
+      const int4 mine = a.xent[x0 + min(lane, nb - 1)];  // lane j holds entry x0 + j
+      double h[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int slot = __shfl_sync(0xffffffffu, mine.x, j);
+        h[j] = (j < nb && live0) ? __ldcg(halo + (size_t)slot * a.n_rows + lane) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < nb) {  // warp-uniform
+          const int dcol = __shfl_sync(0xffffffffu, mine.y, j);
+          const int first = __shfl_sync(0xffffffffu, mine.z, j);
+          const int last = __shfl_sync(0xffffffffu, mine.w, j);
+          acc = first ? h[j] : acc + h[j];
+          if (last) {
+            if (RED) {
+              double v = acc * fscale;
+#pragma unroll
+              for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+              if (lane == 0) part[dcol] = v;
+            } else if (live0) {
+              a.A[fout + dcol] = acc * fscale;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// scheduling words of one launch: one completion counter per (row block,
+// tile)
+size_t sweep_sched_ints(int n_rows, int n_tiles) {
+  return (size_t)n_tiles * ((n_rows + sweep::ROWS * sweep::WPC - 1) / (sweep::ROWS * sweep::WPC));
 }
 
 template <int NQ, int MODE, bool RED = false>
@@ -372,8 +466,10 @@ static cudaError_t launch_sweep_nq(const RegularArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     init = true;
   }
-  dim3 grid((a.n_rows + ROWS * WPC - 1) / (ROWS * WPC), a.n_tiles);
-  k_sweep<NQ, MODE, RED><<<grid, 32 * WPC, smem, st>>>(a);
+  const int nrb = (a.n_rows + ROWS * WPC - 1) / (ROWS * WPC);
+  cudaError_t e = cudaMemsetAsync(a.sched, 0, sweep_sched_ints(a.n_rows, a.n_tiles) * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  k_sweep<NQ, MODE, RED><<<dim3(nrb, a.n_tiles), 32 * WPC, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -66,11 +66,15 @@ int hvb_sweep_geometry(int* out) {
   return HVB_OK;
 }
 
-int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_col0,
-                         const int* tile_width, int n_tiles, int nq, const double* hats, int row_begin, int n_rows,
-                         const double* rowdata, const int* row_col, const double* row_scale,
-                         const long long* row_out, double* A, long long part_ld, const int* tri_cols, int mode,
-                         int* near_list, unsigned long long* near_count, long long near_cap, void* stream) {
+long long hvb_sweep_sched_ints(int n_rows, int n_tiles) { return (long long)hvb::sweep_sched_ints(n_rows, n_tiles); }
+
+int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_lptr,
+                         const int* lcol, const int* tile_xptr, const int* xent, const int* tile_pptr,
+                         const int* prods, const int* tile_cptr, const int* cons, int n_tiles, int nq,
+                         const double* hats, int row_begin, int n_rows, const double* rowdata, const int* row_col,
+                         const double* row_scale, const long long* row_out, double* A, long long part_ld,
+                         const int* tri_cols, int mode, double* halo, int* sched, int* near_list,
+                         unsigned long long* near_count, long long near_cap, void* stream) {
   if (n_rows <= 0 || n_tiles <= 0) return HVB_OK;
   if (part_ld < 0 || (part_ld > 0 && (mode != 1 || row_begin % 32 != 0)))
     return fail(HVB_EARG, "hvb_assemble_regular: charge-reduce mode needs ADL rows starting at a 32-row boundary");
@@ -81,8 +85,18 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
   std::memset(&a, 0, sizeof a);
   a.stream = panel_stream;
   a.tile_ptr = (const int64_t*)tile_ptr;
-  a.tile_col0 = tile_col0;
-  a.tile_width = tile_width;
+  if (!sched || !tile_lptr || !lcol || !tile_xptr || !tile_pptr || !tile_cptr)
+    return fail(HVB_EARG, "hvb_assemble_regular: null schedule");
+  a.tile_lptr = tile_lptr;
+  a.lcol = lcol;
+  a.tile_xptr = tile_xptr;
+  a.xent = (const int4*)xent;
+  a.tile_pptr = tile_pptr;
+  a.prods = prods;
+  a.tile_cptr = tile_cptr;
+  a.cons = cons;
+  a.halo = halo;
+  a.sched = sched;
   a.n_tiles = n_tiles;
   a.row_begin = row_begin;
   a.n_rows = n_rows;

@@ -10,8 +10,16 @@ namespace hvb {
 struct RegularArgs {
   const double* stream;     // tile panel streams (csrc/assemble.cu record formats)
   const int64_t* tile_ptr;  // (n_tiles+1) record offsets
-  const int* tile_col0;     // first device column of each tile
-  const int* tile_width;    // owned columns of each tile
+  const int* tile_lptr;     // (n_tiles+1) local column offsets
+  const int* lcol;          // per local column: device column, or ~slot (halo copy / partial)
+  const int* tile_xptr;     // (n_tiles+1) exchange entry offsets
+  const int4* xent;         // per entry: slot, device column, first, last
+  const int* tile_pptr;     // (n_tiles+1) producer offsets
+  const int* prods;         // distinct producer tiles of each tile
+  const int* tile_cptr;     // (n_tiles+1) consumer offsets
+  const int* cons;          // distinct consumer tiles of each tile
+  double* halo;             // (n_slots, n_rows) exchange slots of this launch
+  int* sched;               // sweep_sched_ints(n_rows, n_tiles): completion counters
   int n_tiles;
   int row_begin;            // first row-list entry of this launch
   int n_rows;               // rows in this launch
@@ -88,6 +96,7 @@ struct FieldArgs {
 cudaError_t launch_regular(const RegularArgs& a, int nq, int mode, cudaStream_t st);
 int sweep_record_doubles(int nq, int mode);
 int sweep_window_stride();
+size_t sweep_sched_ints(int n_rows, int n_tiles);
 void sweep_geometry(int* out);
 cudaError_t launch_build_table(const double* nodes6, int nt, int nq, const double* rule, double* out,
                                cudaStream_t st);

@@ -4,22 +4,34 @@
 // of every assemble() on a fresh mesh.
 //
 //  1. Recursive coordinate bisection of the collocation points (median split
-//     on the longest extent) into tiles of <= max_tile columns.
-//  2. Each tile is swept along its longest axis: its columns are numbered in
-//     that order (the device column order is tile after tile).
-//  3. Records: one per (panel, tile owning >= 1 of its corners); a record
-//     contributes to its owned corners only.  Sorted by (first owned local
-//     column, panel).
-//  4. Stages of GROUP records (one bulk copy each), first-fit in record
+//     on the longest extent) into tiles of <= max_tile columns.  A tile OWNS
+//     its columns; each tile is swept along its longest axis and its owned
+//     columns are numbered in that order (the device column order is tile
+//     after tile).
+//  2. Records: ONE per panel, in its primary tile = the lowest-numbered tile
+//     owning one of its corners, so no panel is evaluated twice.  A tile's
+//     LOCAL columns are its owned columns plus its "halo": corners of its
+//     panels owned by later tiles.  Local columns are numbered along the
+//     sweep axis; records sorted by (first local column, panel).
+//  3. Stages of GROUP records (one bulk copy each), first-fit in record
 //     order: a record joins the oldest open stage whose first record's first
-//     owned column is within `band` of its last owned column and whose owned
+//     local column is within `band` of its last local column and whose
 //     corners are disjoint from its own, else opens a new stage; stages are
 //     emitted in creation order, short ones padded with dummy records (-1).
-//     Disjoint owned corners let the kernel update its window for a whole
-//     stage without read-after-write chains.
-//  5. A tile whose own records span more than `band` columns, or whose
+//     Disjoint corners let the kernel update its window for a whole stage
+//     without read-after-write chains.
+//  4. A tile whose records span more than `band` local columns, or whose
 //     stages pad more than 1/8 of their slots, is halved across its sweep
-//     direction (second-longest axis) and the pass repeats.
+//     direction (second-longest axis) and the pass repeats over all tiles
+//     (tile numbers, hence primaries, move with every split).
+//  5. Halo exchange through slots of raw partial sums (n_rows doubles
+//     each): a producing tile writes its sums of a halo column into the
+//     copy's slot; the owning (later) tile writes its own sums of that
+//     "receiving" column into a partial slot instead of A; the last CTA of
+//     the owner and its producers (same rows) to finish adds partial +
+//     copies (producer order) and writes the entry, so each entry is summed
+//     in a fixed order and no CTA waits.  Receiving columns are numbered
+//     last within their tile, so those writes are contiguous runs of A.
 //
 // Everything is deterministic (ties broken by index).
 #include <algorithm>
@@ -35,12 +47,21 @@ namespace {
 
 struct Tiling {
   std::vector<int> perm;          // device column -> original column
-  std::vector<int> col0, width;   // per tile
+  std::vector<int> col0, width;   // per tile: owned device columns
   std::vector<long long> ptr;     // per tile: record offsets (n_tiles + 1)
   std::vector<int> ent_tri;       // per record: panel (-1: dummy)
-  std::vector<int> ent_meta;      // per record: mfirst, l0, l1, l2, flags (l = owned local column or -1)
+  std::vector<int> ent_meta;      // per record: mfirst, l0, l1, l2, flags (l = local column, -1 dummy)
+  std::vector<int> lptr;          // per tile: local column offsets (n_tiles + 1)
+  std::vector<int> lcol;          // per local column: device column, or ~slot (halo copy / partial)
+  std::vector<int> xptr;          // per tile: exchange entry offsets (n_tiles + 1)
+  std::vector<int> xent;          // per exchange entry: slot, device column, first, last
+  std::vector<int> pptr;          // per tile: producer offsets (n_tiles + 1)
+  std::vector<int> prods;         // per tile: distinct producer tiles, ascending
+  std::vector<int> cptr;          // per tile: consumer offsets (n_tiles + 1)
+  std::vector<int> cons;          // per tile: distinct consumer tiles, ascending
   int band = 0;
   long long real = 0;             // non-dummy records
+  int n_halo = 0, n_slots = 0;
 };
 
 using Pts = const double*;
@@ -85,11 +106,11 @@ void rcb(Pts p, std::vector<int> idx, int max_tile, std::vector<std::vector<int>
 }
 
 struct Rec {
-  int tri, mfirst, mlast, l[3], flags;
+  int tri, mfirst, mlast, l[3];
 };
 
 struct Done {  // one finished tile
-  std::vector<int> cols;      // device order
+  std::vector<int> lcols;     // local columns (original ids), window order
   std::vector<int> ent_tri;   // records (-1: dummy)
   std::vector<int> ent_meta;  // 5 per record
   int band = 0;
@@ -99,47 +120,61 @@ struct Done {  // one finished tile
 struct Ctx {
   Pts p;
   const int* tri_cols;
-  std::vector<int> star_ptr, star_tri;  // vertex -> panels (CSR)
-  std::vector<int> tile_of, local;      // scratch, valid for the tile being processed
-  std::vector<int> seen;                // panel -> last tile stamp
+  const std::vector<int>* star_ptr;
+  const std::vector<int>* star_tri;
+  const std::vector<int>* home;   // column -> owning tile (current numbering)
+  std::vector<int> local, lstamp;  // scratch, valid for the tile being processed
+  std::vector<int> seen;           // panel -> last stamp
   int stamp = 0;
   int band, group;
 };
 
-// Records and stages of one tile; false if the tile must be split (a record
-// spans more than `band` columns, or its stages pad more than 1/8 of slots).
-bool build_tile(Ctx& C, std::vector<int>& cols, Done& out) {
-  sort_along(C.p, cols, longest_axis(C.p, cols));
-  const int k = ++C.stamp;
-  for (int i = 0; i < (int)cols.size(); ++i) {
-    C.tile_of[cols[i]] = k;
-    C.local[cols[i]] = i;
-  }
-  std::vector<Rec> R;
+// Records and stages of tile k (owned columns `cols`, sorted in place along
+// the sweep axis); false if the tile must be split (a record spans more
+// than `band` local columns, or its stages pad more than 1/8 of slots).
+bool build_tile(Ctx& C, int k, std::vector<int>& cols, Done& out) {
+  const int ax = longest_axis(C.p, cols);
+  sort_along(C.p, cols, ax);
+  const std::vector<int>& home = *C.home;
+  const int st = ++C.stamp;
+  std::vector<int> tris, lcols(cols);
+  for (int v : cols) C.lstamp[v] = st;
   for (int v : cols)
-    for (int s = C.star_ptr[v]; s < C.star_ptr[v + 1]; ++s) {
-      const int t = C.star_tri[s];
-      if (C.seen[t] == k) continue;
-      C.seen[t] = k;
+    for (int s = (*C.star_ptr)[v]; s < (*C.star_ptr)[v + 1]; ++s) {
+      const int t = (*C.star_tri)[s];
+      if (C.seen[t] == st) continue;
+      C.seen[t] = st;
       const int* c = C.tri_cols + 3 * (size_t)t;
-      Rec r{t, 1 << 30, -1, {-1, -1, -1}, C.tile_of[c[0]] == k ? 1 : 0};
+      if (std::min(home[c[0]], std::min(home[c[1]], home[c[2]])) != k) continue;  // primary elsewhere
+      tris.push_back(t);
       for (int i = 0; i < 3; ++i)
-        if (C.tile_of[c[i]] == k) {
-          r.l[i] = C.local[c[i]];
-          r.mfirst = std::min(r.mfirst, r.l[i]);
-          r.mlast = std::max(r.mlast, r.l[i]);
+        if (C.lstamp[c[i]] != st) {  // halo: owned by a later tile
+          C.lstamp[c[i]] = st;
+          lcols.push_back(c[i]);
         }
-      if (r.mlast - r.mfirst > C.band) return false;
-      R.push_back(r);
     }
-  std::sort(R.begin(), R.end(), [](const Rec& a, const Rec& b) {
-    return a.mfirst < b.mfirst || (a.mfirst == b.mfirst && a.tri < b.tri);
-  });
+  sort_along(C.p, lcols, ax);
+  for (int i = 0; i < (int)lcols.size(); ++i) C.local[lcols[i]] = i;
+  std::sort(tris.begin(), tris.end());
+  std::vector<Rec> R;
+  R.reserve(tris.size());
+  for (int t : tris) {
+    const int* c = C.tri_cols + 3 * (size_t)t;
+    Rec r{t, 1 << 30, -1, {-1, -1, -1}};
+    for (int i = 0; i < 3; ++i) {
+      r.l[i] = C.local[c[i]];
+      r.mfirst = std::min(r.mfirst, r.l[i]);
+      r.mlast = std::max(r.mlast, r.l[i]);
+    }
+    if (r.mlast - r.mfirst > C.band) return false;
+    R.push_back(r);
+  }
+  std::stable_sort(R.begin(), R.end(), [](const Rec& a, const Rec& b) { return a.mfirst < b.mfirst; });
   // stages, first-fit in record order: a record joins the oldest open stage
-  // it fits (within band of the stage's first record, owned corners
-  // disjoint), else opens a new one; stages are emitted in creation order,
-  // so stage starts never decrease and every record of a later stage has
-  // its first owned column >= this stage's start (the kernel's flush rule)
+  // it fits (within band of the stage's first record, corners disjoint),
+  // else opens a new one; stages are emitted in creation order, so stage
+  // starts never decrease and every record of a later stage has its first
+  // local column >= this stage's start (the kernel's flush rule)
   const int band = C.band, group = C.group;
   std::vector<std::vector<int>> stages;
   std::vector<int> open;  // indices into stages, creation order
@@ -153,7 +188,7 @@ bool build_tile(Ctx& C, std::vector<int>& cols, Done& out) {
       bool clash = false;
       for (int gi : g)
         for (int x = 0; x < 3 && !clash; ++x)
-          for (int y = 0; y < 3 && !clash; ++y) clash = R[gi].l[x] >= 0 && R[gi].l[x] == r.l[y];
+          for (int y = 0; y < 3 && !clash; ++y) clash = R[gi].l[x] == r.l[y];
       if (clash) continue;
       g.push_back(i);
       if ((int)g.size() == group) open.erase(open.begin() + o);
@@ -166,17 +201,17 @@ bool build_tile(Ctx& C, std::vector<int>& cols, Done& out) {
   }
   const size_t slots = (size_t)group * stages.size();
   if (R.size() > 64 && 8 * (slots - R.size()) > slots && cols.size() > 1) return false;
-  out.cols = cols;
+  out.lcols = lcols;
   for (const auto& g : stages) {
     const Rec& r0 = R[g[0]];
     for (int gi : g) {
       const Rec& r = R[gi];
       out.ent_tri.push_back(r.tri);
-      out.ent_meta.insert(out.ent_meta.end(), {r.mfirst, r.l[0], r.l[1], r.l[2], r.flags});
+      out.ent_meta.insert(out.ent_meta.end(), {r.mfirst, r.l[0], r.l[1], r.l[2], 1});
       out.band = std::max(out.band, r.mlast - r0.mfirst);
       ++out.real;
     }
-    for (int d = (int)g.size(); d < group; ++d) {  // dummy: no owned corner, not primary
+    for (int d = (int)g.size(); d < group; ++d) {  // dummy: no corner (window dump slot), never emits
       out.ent_tri.push_back(-1);
       out.ent_meta.insert(out.ent_meta.end(), {r0.mfirst, -1, -1, -1, 0});
     }
@@ -184,105 +219,186 @@ bool build_tile(Ctx& C, std::vector<int>& cols, Done& out) {
   return true;
 }
 
-// depth-first: a tile that must be split is replaced by its two halves
-// (across the sweep direction: the tile stays a strip), in place
-bool process(Ctx& C, std::vector<int> cols, std::vector<Done>& out, int depth) {
-  Done d;
-  if (build_tile(C, cols, d)) {
-    out.push_back(std::move(d));
-    return true;
-  }
-  if (cols.size() <= 1 || depth > 48) return false;  // pathological mesh: band not bounded
-  sort_along(C.p, cols, longest_axis(C.p, cols, 1));
-  const size_t h = cols.size() / 2;
-  std::vector<int> a(cols.begin(), cols.begin() + h), b(cols.begin() + h, cols.end());
-  return process(C, std::move(a), out, depth + 1) && process(C, std::move(b), out, depth + 1);
-}
-
 }  // namespace
 
 extern "C" {
 
 // Returns 0 on success; *handle owns the result until hvb_tiling_free.
-// sizes[0..3] = n_tiles, n_records (incl. dummies), band, real records.
+// sizes[0..8] = n_tiles, n_records (incl. dummies), band, real records,
+// local columns (summed over tiles), exchange entries, slots (halo copies
+// + partials), halo copies, producer entries.
 int hvb_tiling_build(const double* points, int n, const int* tri_cols, int nt, int max_tile, int band, int group,
                      long long* sizes, void** handle) {
   if (!points || !tri_cols || !sizes || !handle || n <= 0 || nt < 0 || max_tile < 1 || band < 0 || group < 1)
     return 1;
   for (long long i = 0; i < 3ll * nt; ++i)
     if (tri_cols[i] < 0 || tri_cols[i] >= n) return 1;
-  Ctx C;
-  C.p = points;
-  C.tri_cols = tri_cols;
-  C.band = band;
-  C.group = group;
-  C.star_ptr.assign(n + 1, 0);
-  for (long long i = 0; i < 3ll * nt; ++i) ++C.star_ptr[tri_cols[i] + 1];
-  for (int v = 0; v < n; ++v) C.star_ptr[v + 1] += C.star_ptr[v];
-  C.star_tri.resize(3 * (size_t)nt);
+  std::vector<int> star_ptr(n + 1, 0), star_tri(3 * (size_t)nt);
+  for (long long i = 0; i < 3ll * nt; ++i) ++star_ptr[tri_cols[i] + 1];
+  for (int v = 0; v < n; ++v) star_ptr[v + 1] += star_ptr[v];
   {
-    std::vector<int> fill(C.star_ptr.begin(), C.star_ptr.end() - 1);
+    std::vector<int> fill(star_ptr.begin(), star_ptr.end() - 1);
     for (int t = 0; t < nt; ++t)
-      for (int j = 0; j < 3; ++j) C.star_tri[fill[tri_cols[3 * (size_t)t + j]]++] = t;
+      for (int j = 0; j < 3; ++j) star_tri[fill[tri_cols[3 * (size_t)t + j]]++] = t;
   }
   std::vector<int> all(n);
   std::iota(all.begin(), all.end(), 0);
   std::vector<std::vector<int>> tiles;
   rcb(points, all, max_tile, tiles);
-  // top-level tiles are independent: one worker thread per tile (each with
-  // its own scratch), results concatenated in tile order
-  const int nw = (int)std::min<size_t>(tiles.size(), std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
-  std::vector<std::vector<Done>> parts(tiles.size());
-  std::vector<char> ok(tiles.size(), 1);
-  std::atomic<size_t> next{0};
-  auto work = [&]() {
-    Ctx W = C;
-    W.tile_of.assign(n, 0);
-    W.local.assign(n, 0);
-    W.seen.assign(nt, 0);
-    for (size_t i; (i = next.fetch_add(1)) < tiles.size();) ok[i] = process(W, std::move(tiles[i]), parts[i], 0);
-  };
-  std::vector<std::thread> pool;
-  for (int w = 1; w < nw; ++w) pool.emplace_back(work);
-  work();
-  for (auto& th : pool) th.join();
+  std::vector<int> home(n);
   std::vector<Done> done;
-  for (size_t i = 0; i < tiles.size(); ++i) {
-    if (!ok[i]) return 2;
-    for (auto& d : parts[i]) done.push_back(std::move(d));
+  const int nw = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  for (int pass = 0;; ++pass) {
+    if (pass > 64) return 2;  // pathological mesh: band not bounded
+    for (size_t k = 0; k < tiles.size(); ++k)
+      for (int v : tiles[k]) home[v] = (int)k;
+    done.assign(tiles.size(), Done());
+    std::vector<char> ok(tiles.size(), 1);
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+      Ctx W;
+      W.p = points;
+      W.tri_cols = tri_cols;
+      W.star_ptr = &star_ptr;
+      W.star_tri = &star_tri;
+      W.home = &home;
+      W.band = band;
+      W.group = group;
+      W.local.assign(n, 0);
+      W.lstamp.assign(n, 0);
+      W.seen.assign(nt, 0);
+      for (size_t i; (i = next.fetch_add(1)) < tiles.size();) ok[i] = build_tile(W, (int)i, tiles[i], done[i]);
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < std::min<int>(nw, (int)tiles.size()); ++w) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+    if (std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; })) break;
+    // halve every failing tile across its sweep direction, in place
+    std::vector<std::vector<int>> next_tiles;
+    for (size_t k = 0; k < tiles.size(); ++k) {
+      if (ok[k] || tiles[k].size() <= 1) {
+        if (!ok[k]) return 2;
+        next_tiles.push_back(std::move(tiles[k]));
+        continue;
+      }
+      std::vector<int>& cols = tiles[k];
+      sort_along(points, cols, longest_axis(points, cols, 1));
+      const size_t h = cols.size() / 2;
+      next_tiles.emplace_back(cols.begin(), cols.begin() + h);
+      next_tiles.emplace_back(cols.begin() + h, cols.end());
+    }
+    tiles.swap(next_tiles);
   }
   Tiling* T = new Tiling();
+  // halo slots in tile order; hl[v] = (slot, producer) of every halo copy of
+  // column v, producers ascending
+  std::vector<std::vector<std::array<int, 2>>> hl(n);
+  for (size_t k = 0; k < tiles.size(); ++k)
+    for (int v : done[k].lcols)
+      if (home[v] != (int)k) hl[v].push_back({T->n_halo++, (int)k});
+  // device columns: per tile its owned columns without halo copies (sweep
+  // order), then the receiving ones (sweep order); a receiving column gets a
+  // "partial" slot (after the halo slots) for its own sums
+  std::vector<int> dev(n), pslot(n, -1);
+  int n_slots = T->n_halo;
   T->ptr.assign(1, 0);
+  T->lptr.assign(1, 0);
+  T->xptr.assign(1, 0);
+  T->pptr.assign(1, 0);
   int c0 = 0;
-  for (auto& d : done) {
-    T->perm.insert(T->perm.end(), d.cols.begin(), d.cols.end());
+  for (size_t k = 0; k < tiles.size(); ++k) {
     T->col0.push_back(c0);
-    T->width.push_back((int)d.cols.size());
-    c0 += (int)d.cols.size();
+    for (int pass2 = 0; pass2 < 2; ++pass2)
+      for (int v : tiles[k])
+        if (hl[v].empty() == (pass2 == 0)) {
+          dev[v] = c0++;
+          T->perm.push_back(v);
+          if (pass2) pslot[v] = n_slots++;
+        }
+    T->width.push_back(c0 - T->col0.back());
+    const Done& d = done[k];
     T->ent_tri.insert(T->ent_tri.end(), d.ent_tri.begin(), d.ent_tri.end());
     T->ent_meta.insert(T->ent_meta.end(), d.ent_meta.begin(), d.ent_meta.end());
     T->ptr.push_back((long long)T->ent_tri.size());
     T->band = std::max(T->band, d.band);
     T->real += d.real;
   }
-  sizes[0] = (long long)done.size();
+  for (size_t k = 0; k < tiles.size(); ++k) {
+    // local columns: device column, or ~slot (halo copy / partial)
+    for (int v : done[k].lcols) {
+      if (home[v] == (int)k) {
+        T->lcol.push_back(pslot[v] < 0 ? dev[v] : ~pslot[v]);
+      } else {
+        int slot = -1;
+        for (const auto& h : hl[v])
+          if (h[1] == (int)k) slot = h[0];
+        T->lcol.push_back(~slot);
+      }
+    }
+    T->lptr.push_back((int)T->lcol.size());
+    // exchange entries of the receiving columns, device order: partial
+    // first, then the halo copies by producer; and the distinct producers
+    std::vector<int> prods;
+    for (int v : tiles[k]) {
+      if (hl[v].empty()) continue;
+      T->xent.insert(T->xent.end(), {pslot[v], dev[v], 1, 0});
+      for (size_t i = 0; i < hl[v].size(); ++i) {
+        T->xent.insert(T->xent.end(), {hl[v][i][0], dev[v], 0, i + 1 == hl[v].size() ? 1 : 0});
+        prods.push_back(hl[v][i][1]);
+      }
+    }
+    std::sort(prods.begin(), prods.end());
+    prods.erase(std::unique(prods.begin(), prods.end()), prods.end());
+    T->prods.insert(T->prods.end(), prods.begin(), prods.end());
+    T->pptr.push_back((int)T->prods.size());
+    T->xptr.push_back((int)(T->xent.size() / 4));
+  }
+  // consumers: the transpose of the producer lists
+  {
+    std::vector<std::vector<int>> cl(tiles.size());
+    for (size_t k = 0; k < tiles.size(); ++k)
+      for (int i = T->pptr[k]; i < T->pptr[k + 1]; ++i) cl[T->prods[i]].push_back((int)k);
+    T->cptr.assign(1, 0);
+    for (auto& c : cl) {
+      T->cons.insert(T->cons.end(), c.begin(), c.end());
+      T->cptr.push_back((int)T->cons.size());
+    }
+  }
+  T->n_slots = n_slots;
+  sizes[0] = (long long)tiles.size();
   sizes[1] = (long long)T->ent_tri.size();
   sizes[2] = T->band;
   sizes[3] = T->real;
+  sizes[4] = T->lptr.back();
+  sizes[5] = T->xptr.back();
+  sizes[6] = T->n_slots;
+  sizes[7] = T->n_halo;
+  sizes[8] = T->pptr.back();
   *handle = T;
   return 0;
 }
 
 int hvb_tiling_fetch(void* handle, int* perm, int* tile_col0, int* tile_width, long long* tile_ptr, int* ent_tri,
-                     int* ent_meta) {
+                     int* ent_meta, int* tile_lptr, int* lcol, int* tile_xptr, int* xent, int* tile_pptr,
+                     int* prods, int* tile_cptr, int* cons) {
   if (!handle) return 1;
   const Tiling* T = static_cast<const Tiling*>(handle);
-  std::memcpy(perm, T->perm.data(), T->perm.size() * sizeof(int));
-  std::memcpy(tile_col0, T->col0.data(), T->col0.size() * sizeof(int));
-  std::memcpy(tile_width, T->width.data(), T->width.size() * sizeof(int));
+  auto put = [](int* dst, const std::vector<int>& v) { std::memcpy(dst, v.data(), v.size() * sizeof(int)); };
+  put(perm, T->perm);
+  put(tile_col0, T->col0);
+  put(tile_width, T->width);
   std::memcpy(tile_ptr, T->ptr.data(), T->ptr.size() * sizeof(long long));
-  std::memcpy(ent_tri, T->ent_tri.data(), T->ent_tri.size() * sizeof(int));
-  std::memcpy(ent_meta, T->ent_meta.data(), T->ent_meta.size() * sizeof(int));
+  put(ent_tri, T->ent_tri);
+  put(ent_meta, T->ent_meta);
+  put(tile_lptr, T->lptr);
+  put(lcol, T->lcol);
+  put(tile_xptr, T->xptr);
+  put(xent, T->xent);
+  put(tile_pptr, T->pptr);
+  put(prods, T->prods);
+  put(tile_cptr, T->cptr);
+  put(cons, T->cons);
   return 0;
 }
 

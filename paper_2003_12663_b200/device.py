@@ -4,15 +4,17 @@ Host side (NumPy, once per mesh):
 
 * ``column_tiling`` -- the matrix is stored in a *device column order*:
   recursive coordinate bisection of the collocation points into compact
-  column tiles, each swept along its longest axis.  A panel that touches a
-  tile contributes to its *owned* corners only; within a tile the owned
-  corners of every aligned group of GROUP consecutive records lie within
-  ``band`` columns of the group's first owned column, which is what lets
-  the assembly warp keep a WINDOW-column sliding window of running sums
-  (csrc/assemble.cu, sweep_geometry(): WINDOW 48, flushes of 16 columns, band 32).
-  Panels with corners in several tiles are evaluated once per tile
-  (``redundancy``, 1.14 at config 4).
-* entries (tile, panel) sorted by (tile, first owned column).
+  column tiles, each swept along its longest axis (csrc/tiling.cpp).  Every
+  panel is evaluated once, in the lowest-numbered tile owning one of its
+  corners; its corners owned by later tiles are that tile's *halo* columns,
+  whose partial sums the owning tile imports (fixed order) before writing
+  them.  Within a tile the corners of every stage of GROUP consecutive
+  records lie within ``band`` columns of the stage's first column, which is
+  what lets the assembly warp keep a WINDOW-column sliding window of running
+  sums (csrc/assemble.cu, sweep_geometry(): WINDOW 64, flushes of 16
+  columns, band 48).  ``redundancy`` = local columns per device column
+  (1.15 at config 4: the halo).
+* records (tile, panel) sorted by (tile, first local column).
 * ``panel_groups`` -- bounds of aligned 32-panel groups for the N-body and
   surface-distance kernels.
 
@@ -61,6 +63,16 @@ class ColumnTiling:
     tile_col0: np.ndarray   # (n_tiles,)
     tile_width: np.ndarray  # (n_tiles,)
     tile_ptr: np.ndarray    # (n_tiles+1,) entry offsets
+    tile_lptr: np.ndarray   # (n_tiles+1,) local column offsets
+    lcol: np.ndarray        # (n_local,): device column, or ~slot (halo copy / partial)
+    tile_xptr: np.ndarray   # (n_tiles+1,) exchange entry offsets
+    xent: np.ndarray        # (n_xent, 4): slot, device column, first, last
+    tile_pptr: np.ndarray   # (n_tiles+1,) producer offsets
+    prods: np.ndarray       # distinct producer tiles per tile
+    tile_cptr: np.ndarray   # (n_tiles+1,) consumer offsets
+    cons: np.ndarray        # distinct consumer tiles per tile
+    n_slots: int            # halo copies + partials
+    n_halo: int
     ent_tri: np.ndarray     # (ne,) panel of each entry
     ent_meta: np.ndarray    # (ne, 5): mfirst, l0, l1, l2, flags
     band: int
@@ -71,12 +83,17 @@ def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = MAX_
                   group: int | None = None) -> ColumnTiling:
     """Column tiles + grouped (tile, panel) records, built natively
     (csrc/tiling.cpp, host C++): recursive coordinate bisection into tiles
-    of <= max_tile columns swept along their longest axis; records sorted by
-    first owned column and grouped in stages of ``group`` whose owned corners
-    are disjoint and lie within ``band_max`` columns of the stage's first
-    record (short stages padded with dummy records, panel -1); tiles whose
-    records span more than ``band_max`` columns are halved across their sweep
-    direction.  ``redundancy`` = real records per panel."""
+    of <= max_tile owned columns swept along their longest axis; one record
+    per panel, in the lowest-numbered tile owning one of its corners; a
+    tile's local columns (owned + halo: its panels' corners owned by later
+    tiles) numbered along the sweep axis; records sorted by first local
+    column and grouped in stages of ``group`` whose corners are disjoint and
+    lie within ``band_max`` columns of the stage's first record (short
+    stages padded with dummy records, panel -1); tiles whose records span
+    more than ``band_max`` columns are halved across their sweep direction.
+    Halo partial sums travel through slots to the owning tile, which sums
+    its own partial and the copies in producer order (``xent``).
+    ``redundancy`` = local columns per device column."""
     import ctypes
 
     win, flush, grp, _ = sweep_geometry()
@@ -86,29 +103,41 @@ def column_tiling(points: np.ndarray, tri_cols: np.ndarray, max_tile: int = MAX_
     tc = np.ascontiguousarray(tri_cols, dtype=np.int32)
     n, nt = len(pts), len(tc)
     h = _lib.lib()
-    sizes = np.zeros(4, dtype=np.int64)
+    sizes = np.zeros(9, dtype=np.int64)
     handle = ctypes.c_void_p()
     rc = h.hvb_tiling_build(pts.ctypes.data_as(ctypes.c_void_p), n, tc.ctypes.data_as(ctypes.c_void_p), nt,
                             int(max_tile), int(band_max), int(group), sizes.ctypes.data_as(ctypes.c_void_p),
                             ctypes.byref(handle))
     if rc != 0:
         raise RuntimeError("column tiling failed" + (": could not bound the panel band" if rc == 2 else ""))
-    n_tiles, ne, band, real = (int(x) for x in sizes)
+    n_tiles, ne, band, real, n_local, n_x, n_slots, n_halo, n_prod = (int(x) for x in sizes)
     perm = np.empty(n, dtype=np.int32)
     col0 = np.empty(n_tiles, dtype=np.int32)
     width = np.empty(n_tiles, dtype=np.int32)
     ptr = np.empty(n_tiles + 1, dtype=np.int64)
     ent_tri = np.empty(ne, dtype=np.int32)
     ent_meta = np.empty((ne, 5), dtype=np.int32)
+    lptr = np.empty(n_tiles + 1, dtype=np.int32)
+    lcol = np.empty(n_local, dtype=np.int32)
+    xptr = np.empty(n_tiles + 1, dtype=np.int32)
+    xent = np.empty((n_x, 4), dtype=np.int32)
+    pptr = np.empty(n_tiles + 1, dtype=np.int32)
+    prods = np.empty(n_prod, dtype=np.int32)
+    cptr = np.empty(n_tiles + 1, dtype=np.int32)
+    cons = np.empty(n_prod, dtype=np.int32)
     try:
         h.hvb_tiling_fetch(handle, *(a.ctypes.data_as(ctypes.c_void_p) for a in (perm, col0, width, ptr, ent_tri,
-                                                                                 ent_meta)))
+                                                                                 ent_meta, lptr, lcol, xptr, xent,
+                                                                                 pptr, prods, cptr, cons)))
     finally:
         h.hvb_tiling_free(handle)
     inv = np.empty(n, dtype=np.int64)
     inv[perm] = np.arange(n)
     return ColumnTiling(perm=perm.astype(np.int64), inv=inv, tile_col0=col0, tile_width=width, tile_ptr=ptr,
-                        ent_tri=ent_tri, ent_meta=ent_meta, band=band, redundancy=real / max(1, nt))
+                        tile_lptr=lptr, lcol=lcol, tile_xptr=xptr, xent=xent, tile_pptr=pptr, prods=prods,
+                        tile_cptr=cptr, cons=cons,
+                        n_slots=n_slots, n_halo=n_halo,
+                        ent_tri=ent_tri, ent_meta=ent_meta, band=band, redundancy=n_local / max(1, n))
 
 
 def _rule4(rule) -> np.ndarray:
@@ -179,8 +208,15 @@ class DeviceMesh:
         self.perm = up(tiling.perm, **i32)
         self.col_dev = up(tiling.inv, **i32)
         self.tile_ptr = up(tiling.tile_ptr, dtype=torch.int64, device=device)
-        self.tile_col0 = up(tiling.tile_col0, **i32)
-        self.tile_width = up(tiling.tile_width, **i32)
+        self.tile_lptr = up(tiling.tile_lptr, **i32)
+        self.lcol = up(tiling.lcol, **i32)
+        self.tile_xptr = up(tiling.tile_xptr, **i32)
+        self.xent = up(tiling.xent, **i32)
+        self.tile_pptr = up(tiling.tile_pptr, **i32)
+        self.prods = up(tiling.prods, **i32)
+        self.tile_cptr = up(tiling.tile_cptr, **i32)
+        self.cons = up(tiling.cons, **i32)
+        self.n_slots = tiling.n_slots
         self._ent_tri = up(tiling.ent_tri, **i32)
         self._ent_meta = up(tiling.ent_meta, **i32)  # (mfirst, l0, l1, l2, flags); slots = l % WINDOW on the device
         self.n_entries = len(tiling.ent_tri)
@@ -190,6 +226,18 @@ class DeviceMesh:
         self.stream_for(0)  # SL rows; the ADL stream is built on first use
         self.n_tiles = len(tiling.tile_width)
         self.h2d_bytes = int(sum(h2d))
+
+    def sweep_slots(self, n_doubles: int):
+        """Exchange-slot scratch of the regular sweep (csrc/tiling.cpp 5),
+        kept across assemblies (grown on demand): the allocation is tens of
+        GB at config 4 and must not be re-made per call."""
+        import torch
+
+        buf = getattr(self, "_slots", None)
+        if buf is None or buf.numel() < n_doubles:
+            self._slots = None
+            buf = self._slots = torch.empty(max(1, n_doubles), dtype=torch.float64, device=self.device)
+        return buf
 
     def stream_for(self, mode: int):
         """Packed panel stream of the regular sweep: mode 0 (SL rows) or 1

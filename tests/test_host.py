@@ -22,7 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _header_functions():
     text = open(os.path.join(ROOT, "include", "hvb.h")).read()
-    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(hvb_\w+)\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|long long|const char\*)\s+(hvb_\w+)\(", text, flags=re.M)))
 
 
 def test_library_exports_every_header_symbol():
@@ -45,7 +45,7 @@ def test_binding_signatures_cover_header():
 
     declared = set(_header_functions()) - {"hvb_last_error", "hvb_version", "hvb_line_state_bytes",
                                            "hvb_mgs_partial_size", "hvb_ipc_handle_bytes",
-                                           "hvb_stream_record_doubles"}
+                                           "hvb_stream_record_doubles", "hvb_sweep_sched_ints"}
     assert declared == set(_lib.SIGNATURES)
 
 
@@ -399,32 +399,40 @@ def test_import_alias_drop_in():
                                    lambda: fixtures.rod_plane_mesh(0.12), lambda: fixtures.rod_plane_mesh(0.4)])
 def test_column_tiling_invariants(maker):
     """csrc/tiling.cpp (host C++, no GPU): the device column order is a
-    permutation; every (panel, tile owning one of its corners) record exists
-    once with its owned corners; stages of `group` records have pairwise
-    disjoint owned columns within the band (window - flush) of their first
-    record, whose
-    first owned column is the stage minimum; stage starts never decrease
-    within a tile; dummies (-1) only pad stages."""
+    permutation of contiguous owned tiles; every panel has exactly one
+    record, in the lowest-numbered tile owning one of its corners, whose
+    corners are that tile's local columns (owned -> device column or the
+    partial slot of a receiving column, halo -> a copy slot); stages of
+    `group` records have pairwise disjoint corners within the band (window
+    - flush) of their first record, whose first column is the stage
+    minimum; stage starts never decrease within a tile; dummies (-1) only
+    pad stages; the receiving columns of a tile are numbered last and their
+    exchange entries are partial then copies in producer order."""
     from paper_2003_12663_b200 import device
 
     m = maker()
     win, flush, grp, _ = device.sweep_geometry()
     band = win - flush
     T = device.column_tiling(m.colloc_points, m.tri_corner_cols, max_tile=2048)
-    n = m.n_collocation
+    n, nt = m.n_collocation, m.n_triangles
+    ntile = len(T.tile_width)
     assert np.array_equal(np.sort(T.perm), np.arange(n))
-    assert T.tile_col0[0] == 0 and T.tile_col0[-1] + T.tile_width[-1] == n
-    tile_of = np.repeat(np.arange(len(T.tile_width)), T.tile_width)[T.inv]
-    local = T.inv - T.tile_col0[tile_of]
-    seen = set()
-    for k in range(len(T.tile_width)):
+    assert np.array_equal(T.tile_col0, np.concatenate([[0], np.cumsum(T.tile_width)[:-1]]))
+    assert T.tile_col0[-1] + T.tile_width[-1] == n
+    home = np.repeat(np.arange(ntile), T.tile_width)[T.inv]          # original col -> owning tile
+    primary = home[m.tri_corner_cols].min(axis=1)
+    copies = {}                                                      # original col -> [(slot, producer)]
+    partial = {}                                                     # original col -> partial slot
+    seen = np.zeros(nt, dtype=int)
+    for k in range(ntile):
+        lc = T.lcol[T.tile_lptr[k]:T.tile_lptr[k + 1]]
         a, b = int(T.tile_ptr[k]), int(T.tile_ptr[k + 1])
         assert (b - a) % grp == 0
         prev = -1
         for s0 in range(a, b, grp):
             st = range(s0, s0 + grp)
             cols = [c for e in st for c in T.ent_meta[e, 1:4] if c >= 0]
-            assert len(cols) == len(set(cols))                       # disjoint owned corners
+            assert len(cols) == len(set(cols))                       # disjoint corners
             start = T.ent_meta[s0, 0]
             assert T.ent_tri[s0] >= 0 and start >= prev
             prev = start
@@ -433,16 +441,50 @@ def test_column_tiling_invariants(maker):
                 if t < 0:
                     assert np.all(T.ent_meta[e, 1:4] == -1) and T.ent_meta[e, 4] == 0
                     continue
-                own = [c for c in T.ent_meta[e, 1:4] if c >= 0]
-                assert min(own) == T.ent_meta[e, 0] >= start and max(own) <= start + band
-                corners = m.tri_corner_cols[t]
-                exp = [int(local[c]) if tile_of[c] == k else -1 for c in corners]
-                assert list(T.ent_meta[e, 1:4]) == exp
-                assert T.ent_meta[e, 4] == int(tile_of[corners[0]] == k)
-                assert (t, k) not in seen
-                seen.add((t, k))
-    want = {(t, int(tile_of[c])) for t in range(m.n_triangles) for c in m.tri_corner_cols[t]}
-    assert seen == want
+                assert primary[t] == k and T.ent_meta[e, 4] == 1
+                loc = T.ent_meta[e, 1:4]
+                assert min(loc) == T.ent_meta[e, 0] >= start and max(loc) <= start + band
+                seen[t] += 1
+        # local columns: every owned column, plus the halo
+        owned = set(T.perm[T.tile_col0[k]:T.tile_col0[k] + T.tile_width[k]].tolist())
+        for e in range(a, b):
+            if T.ent_tri[e] >= 0:
+                for c, l in zip(m.tri_corner_cols[T.ent_tri[e]], T.ent_meta[e, 1:4]):
+                    d = int(lc[l])
+                    if home[c] == k:
+                        assert (d >= 0 and T.perm[d] == c) or (d < 0 and partial.setdefault(int(c), ~d) == ~d)
+                    else:
+                        assert d < 0 and home[c] > k and ~d < T.n_halo
+                        if (~d, k) not in copies.setdefault(int(c), []):
+                            copies[int(c)].append((~d, k))
+        assert sum(1 for d in lc if d >= 0 or ~d >= T.n_halo) == len(owned)
+    assert np.all(seen == 1)
+    # partial slots per receiving column, from the exchange entries (a column
+    # whose own tile has no panel on it is reached through them only)
+    first = T.xent[T.xent[:, 2] == 1]
+    px = {int(T.perm[d]): int(sl) for sl, d, _, _ in first}
+    assert all(px[c] == sl for c, sl in partial.items())
+    partial = px
+    assert set(partial) == set(copies) and len(set(partial.values())) == len(partial)
+    assert all(T.n_halo <= p < T.n_slots for p in partial.values())
+    assert sum(len(v) for v in copies.values()) == T.n_halo
+    for k in range(ntile):
+        x = T.xent[T.tile_xptr[k]:T.tile_xptr[k + 1]]
+        recv = [c for c in T.perm[T.tile_col0[k]:T.tile_col0[k] + T.tile_width[k]] if int(c) in partial]
+        dev = T.inv[recv]
+        assert np.array_equal(dev, np.arange(T.tile_col0[k] + T.tile_width[k] - len(recv),
+                                             T.tile_col0[k] + T.tile_width[k]))  # receiving columns last
+        want = []
+        for c in recv:
+            cp = sorted(copies[int(c)], key=lambda sp: sp[1])
+            want.append([partial[int(c)], T.inv[c], 1, 0])
+            want += [[sl, T.inv[c], 0, int(i + 1 == len(cp))] for i, (sl, _) in enumerate(cp)]
+        assert np.array_equal(x, np.array(want, dtype=np.int32).reshape(-1, 4))
+        prods = sorted({p for c in recv for _, p in copies[int(c)]})
+        assert list(T.prods[T.tile_pptr[k]:T.tile_pptr[k + 1]]) == prods and all(p < k for p in prods)
+        for p in prods:
+            assert k in T.cons[T.tile_cptr[p]:T.tile_cptr[p + 1]]
+    assert len(T.cons) == len(T.prods)
 
 
 # ---------------------------------------------------------------------------

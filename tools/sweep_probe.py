@@ -24,5 +24,5 @@ for _ in range(3):
     reg = sum(e0.elapsed_time(e1) for lab, e0, e1 in prof if lab == "regular") / 1e3
     best = reg if best is None else min(best, reg)
     del A
-print(f"geometry {sweep_geometry()} tiles {dm.n_tiles} records {dm.n_entries} redundancy {dm.tiling.redundancy:.3f} "
+print(f"geometry {sweep_geometry()} tiles {dm.n_tiles} records {dm.n_entries} local/n {dm.tiling.redundancy:.3f} halo {dm.tiling.n_halo} slots {dm.n_slots} "
       f"regular {best * 1e3:.1f} ms")
