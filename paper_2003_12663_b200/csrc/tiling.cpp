@@ -22,8 +22,10 @@
 //     without read-after-write chains.
 //  4. A tile whose records span more than `band` local columns, or whose
 //     stages pad more than 1/8 of their slots, is halved across its sweep
-//     direction (second-longest axis) and the pass repeats over all tiles
-//     (tile numbers, hence primaries, move with every split).
+//     direction (second-longest axis); the halves are built in the next
+//     pass (halving keeps the order of the other tiles, so their primaries
+//     and builds stand).  Before any build, tiles are halved while the span
+//     over their owned columns alone exceeds the band (a cheap lower bound).
 //  5. Halo exchange through slots of raw partial sums (n_rows doubles
 //     each): a producing tile writes its sums of a halo column into the
 //     copy's slot; the owning (later) tile writes its own sums of that
@@ -66,40 +68,95 @@ struct Tiling {
 
 using Pts = const double*;
 
-int longest_axis(Pts p, const std::vector<int>& idx, int rank = 0) {
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  for (int v : idx)
-    for (int d = 0; d < 3; ++d) {
-      lo[d] = std::min(lo[d], p[3 * (size_t)v + d]);
-      hi[d] = std::max(hi[d], p[3 * (size_t)v + d]);
+// Global order of the columns along each axis: (x_a, x_a+1, x_a+2, index)
+// lexicographic on the coordinates rounded to float -- gr[a][v] is column
+// v's position.  A tile keeps its
+// columns sorted along all three axes, so cutting it is a linear stable
+// partition and no tile is ever sorted again.
+// stable LSD radix sort of idx by coordinate ax rounded to float (the
+// order-preserving 32-bit image; 11-bit digits, digits shared by all keys
+// skipped; -0 == +0)
+void radix_sort_along(Pts p, std::vector<int>& idx, int ax) {
+  const size_t m = idx.size();
+  std::vector<uint32_t> key(m), key2(m);
+  std::vector<int> idx2(m);
+  for (size_t i = 0; i < m; ++i) {
+    float x = (float)p[3 * (size_t)idx[i] + ax];
+    if (x == 0.0f) x = 0.0f;
+    uint32_t b;
+    std::memcpy(&b, &x, 4);
+    key[i] = (b >> 31) ? ~b : (b | (1u << 31));
+  }
+  constexpr int DIG = 11, NB = 1 << DIG;
+  std::vector<size_t> cnt(NB);
+  for (int sh = 0; sh < 32; sh += DIG) {
+    std::fill(cnt.begin(), cnt.end(), 0);
+    for (size_t i = 0; i < m; ++i) ++cnt[(key[i] >> sh) & (NB - 1)];
+    if (*std::max_element(cnt.begin(), cnt.end()) == m) continue;  // one digit value: order unchanged
+    size_t run = 0;
+    for (int d = 0; d < NB; ++d) {
+      const size_t c = cnt[d];
+      cnt[d] = run;
+      run += c;
     }
+    for (size_t i = 0; i < m; ++i) {
+      const size_t o = cnt[(key[i] >> sh) & (NB - 1)]++;
+      key2[o] = key[i];
+      idx2[o] = idx[i];
+    }
+    key.swap(key2);
+    idx.swap(idx2);
+  }
+}
+
+struct Order {
+  std::array<std::vector<int>, 3> gr;
+};
+
+struct Tile {
+  std::array<std::vector<int>, 3> by;  // columns in global order along each axis
+  size_t size() const { return by[0].size(); }
+};
+
+// axes by extent descending (ties by axis index): rank 0 = the sweep axis
+int longest_axis(Pts p, const Tile& t, int rank = 0) {
+  double ext[3];
+  for (int d = 0; d < 3; ++d)
+    ext[d] = t.size() ? p[3 * (size_t)t.by[d].back() + d] - p[3 * (size_t)t.by[d].front() + d] : 0.0;
   std::array<int, 3> ax = {0, 1, 2};
-  // extents descending, ties by axis index
-  std::stable_sort(ax.begin(), ax.end(), [&](int a, int b) { return hi[a] - lo[a] > hi[b] - lo[b]; });
+  std::stable_sort(ax.begin(), ax.end(), [&](int a, int b) { return ext[a] > ext[b]; });
   return ax[rank];
 }
 
-// stable sort along axis ax: ties (structured grids share coordinates)
-// keep the order of the previous split or sweep, which keeps equal-coordinate
-// rows geometrically coherent
-void sort_along(Pts p, std::vector<int>& idx, int ax) {
-  std::stable_sort(idx.begin(), idx.end(),
-                   [&](int a, int b) { return p[3 * (size_t)a + ax] < p[3 * (size_t)b + ax]; });
+// halve t along axis a (first half: the lower positions along a)
+void halve(const Tile& t, int a, Tile& lo, Tile& hi, std::vector<int>& mark, int& stamp) {
+  const size_t h = t.size() / 2;
+  const int st = ++stamp;
+  lo.by[a].assign(t.by[a].begin(), t.by[a].begin() + h);
+  hi.by[a].assign(t.by[a].begin() + h, t.by[a].end());
+  for (int v : lo.by[a]) mark[v] = st;
+  for (int d = 0; d < 3; ++d) {
+    if (d == a) continue;
+    lo.by[d].clear();
+    hi.by[d].clear();
+    lo.by[d].reserve(h);
+    hi.by[d].reserve(t.size() - h);
+    for (int v : t.by[d]) (mark[v] == st ? lo : hi).by[d].push_back(v);
+  }
 }
 
-void rcb(Pts p, std::vector<int> idx, int max_tile, std::vector<std::vector<int>>& out) {
-  std::vector<std::vector<int>> stack;
-  stack.push_back(std::move(idx));
+void rcb(Pts p, Tile all, int max_tile, std::vector<Tile>& out, std::vector<int>& mark, int& stamp) {
+  std::vector<Tile> stack;
+  stack.push_back(std::move(all));
   while (!stack.empty()) {
-    std::vector<int> cur = std::move(stack.back());
+    Tile cur = std::move(stack.back());
     stack.pop_back();
     if ((int)cur.size() <= max_tile) {
       out.push_back(std::move(cur));
       continue;
     }
-    sort_along(p, cur, longest_axis(p, cur));
-    const size_t h = cur.size() / 2;
-    std::vector<int> a(cur.begin(), cur.begin() + h), b(cur.begin() + h, cur.end());
+    Tile a, b;
+    halve(cur, longest_axis(p, cur), a, b, mark, stamp);
     stack.push_back(std::move(b));  // second half pushed first: tiles come out in sweep order
     stack.push_back(std::move(a));
   }
@@ -119,6 +176,7 @@ struct Done {  // one finished tile
 
 struct Ctx {
   Pts p;
+  const Order* ord;
   const int* tri_cols;
   const std::vector<int>* star_ptr;
   const std::vector<int>* star_tri;
@@ -132,12 +190,13 @@ struct Ctx {
 // Records and stages of tile k (owned columns `cols`, sorted in place along
 // the sweep axis); false if the tile must be split (a record spans more
 // than `band` local columns, or its stages pad more than 1/8 of slots).
-bool build_tile(Ctx& C, int k, std::vector<int>& cols, Done& out) {
-  const int ax = longest_axis(C.p, cols);
-  sort_along(C.p, cols, ax);
+bool build_tile(Ctx& C, int k, const Tile& tile, Done& out) {
+  const int ax = longest_axis(C.p, tile);
+  const std::vector<int>& cols = tile.by[ax];
+  const std::vector<int>& g = C.ord->gr[ax];
   const std::vector<int>& home = *C.home;
   const int st = ++C.stamp;
-  std::vector<int> tris, lcols(cols);
+  std::vector<int> tris, halo;
   for (int v : cols) C.lstamp[v] = st;
   for (int v : cols)
     for (int s = (*C.star_ptr)[v]; s < (*C.star_ptr)[v + 1]; ++s) {
@@ -150,10 +209,14 @@ bool build_tile(Ctx& C, int k, std::vector<int>& cols, Done& out) {
       for (int i = 0; i < 3; ++i)
         if (C.lstamp[c[i]] != st) {  // halo: owned by a later tile
           C.lstamp[c[i]] = st;
-          lcols.push_back(c[i]);
+          halo.push_back(c[i]);
         }
     }
-  sort_along(C.p, lcols, ax);
+  // local columns: owned and halo merged in the global order along ax
+  std::sort(halo.begin(), halo.end(), [&](int a, int b) { return g[a] < g[b]; });
+  std::vector<int> lcols(cols.size() + halo.size());
+  std::merge(cols.begin(), cols.end(), halo.begin(), halo.end(), lcols.begin(),
+             [&](int a, int b) { return g[a] < g[b]; });
   for (int i = 0; i < (int)lcols.size(); ++i) C.local[lcols[i]] = i;
   std::sort(tris.begin(), tris.end());
   std::vector<Rec> R;
@@ -219,6 +282,29 @@ bool build_tile(Ctx& C, int k, std::vector<int>& cols, Done& out) {
   return true;
 }
 
+// Widest span of the tile's panels over its owned columns numbered along
+// its longest axis (halo corners ignored: a lower bound of the span the
+// build checks against the band).
+int owned_span(Pts p, const int* tri_cols, const std::vector<int>& star_ptr, const std::vector<int>& star_tri,
+               std::vector<int>& rank, const Tile& tile) {
+  const std::vector<int>& cols = tile.by[longest_axis(p, tile)];
+  for (int i = 0; i < (int)cols.size(); ++i) rank[cols[i]] = i + 1;
+  int span = 0;
+  for (int v : cols)
+    for (int s = star_ptr[v]; s < star_ptr[v + 1]; ++s) {
+      const int* c = tri_cols + 3 * (size_t)star_tri[s];
+      int lo = 1 << 30, hi = -1;
+      for (int i = 0; i < 3; ++i)
+        if (rank[c[i]] > 0) {
+          lo = std::min(lo, rank[c[i]]);
+          hi = std::max(hi, rank[c[i]]);
+        }
+      span = std::max(span, hi - lo);
+    }
+  for (int v : cols) rank[v] = 0;
+  return span;
+}
+
 }  // namespace
 
 extern "C" {
@@ -241,55 +327,150 @@ int hvb_tiling_build(const double* points, int n, const int* tri_cols, int nt, i
     for (int t = 0; t < nt; ++t)
       for (int j = 0; j < 3; ++j) star_tri[fill[tri_cols[3 * (size_t)t + j]]++] = t;
   }
-  std::vector<int> all(n);
-  std::iota(all.begin(), all.end(), 0);
-  std::vector<std::vector<int>> tiles;
-  rcb(points, all, max_tile, tiles);
-  std::vector<int> home(n);
-  std::vector<Done> done;
   const int nw = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  // global order along each axis (three sorts in parallel)
+  Order ord;
+  Tile all;
+  {
+    std::vector<std::thread> th;
+    for (int a = 0; a < 3; ++a)
+      th.emplace_back([&, a]() {
+        std::vector<int>& o = all.by[a];
+        o.resize(n);
+        std::iota(o.begin(), o.end(), 0);
+        for (int r = 2; r >= 0; --r) radix_sort_along(points, o, (a + r) % 3);  // (x_a, x_a+1, x_a+2) lexicographic
+        ord.gr[a].resize(n);
+        for (int i = 0; i < n; ++i) ord.gr[a][o[i]] = i;
+      });
+    for (auto& t : th) t.join();
+  }
+  std::vector<int> mark(n, 0);
+  int stamp = 0;
+  std::vector<Tile> tiles;
+  rcb(points, std::move(all), max_tile, tiles, mark, stamp);
+  // Cut tile k across its sweep direction (in place in the tile list).
+  auto cut = [&](std::vector<Tile>& out, Tile& t) {
+    Tile a, b;
+    halve(t, longest_axis(points, t, 1), a, b, mark, stamp);
+    out.push_back(std::move(a));
+    out.push_back(std::move(b));
+  };
+  // presplit, level by level in parallel: a tile whose owned span exceeds
+  // the band is halved across its sweep direction, and the halves checked
+  {
+    std::vector<std::vector<int>> ranks(nw);
+    std::vector<int> span(tiles.size(), 0);
+    std::vector<char> checked(tiles.size(), 0);
+    for (int level = 0; level < 48; ++level) {
+      std::vector<size_t> todo;
+      for (size_t k = 0; k < tiles.size(); ++k)
+        if (!checked[k]) todo.push_back(k);
+      if (todo.empty()) break;
+      std::atomic<size_t> next{0};
+      auto work = [&](int w) {
+        std::vector<int>& rank = ranks[w];
+        if (rank.empty()) rank.assign(n, 0);
+        for (size_t i; (i = next.fetch_add(1)) < todo.size();) {
+          const size_t k = todo[i];
+          span[k] = tiles[k].size() <= 1 ? 0 : owned_span(points, tri_cols, star_ptr, star_tri, rank, tiles[k]);
+          checked[k] = 1;
+        }
+      };
+      std::vector<std::thread> pool;
+      for (int w = 1; w < std::min<int>(nw, (int)todo.size()); ++w) pool.emplace_back(work, w);
+      work(0);
+      for (auto& th : pool) th.join();
+      std::vector<Tile> nt_tiles;
+      std::vector<int> nt_span;
+      std::vector<char> nt_checked;
+      for (size_t k = 0; k < tiles.size(); ++k) {
+        if (span[k] <= band) {
+          nt_tiles.push_back(std::move(tiles[k]));
+          nt_span.push_back(span[k]);
+          nt_checked.push_back(1);
+          continue;
+        }
+        cut(nt_tiles, tiles[k]);
+        nt_span.insert(nt_span.end(), {0, 0});
+        nt_checked.insert(nt_checked.end(), {0, 0});
+      }
+      tiles.swap(nt_tiles);
+      span.swap(nt_span);
+      checked.swap(nt_checked);
+    }
+  }
+  std::vector<int> home(n);
+  std::vector<Done> done(tiles.size());
+  std::vector<char> built(tiles.size(), 0), ok(tiles.size(), 0);
+  std::vector<Ctx> ctx(nw);
+  for (Ctx& W : ctx) {
+    W.p = points;
+    W.ord = &ord;
+    W.tri_cols = tri_cols;
+    W.star_ptr = &star_ptr;
+    W.star_tri = &star_tri;
+    W.home = &home;
+    W.band = band;
+    W.group = group;
+  }
+  // Passes: build the tiles not built yet, halve the failing ones in place.
+  // Halving tile s keeps the relative order of all others, so a panel not
+  // touching s keeps its primary tile and every other tile's build stands;
+  // only the two halves are (re)built in the next pass.
   for (int pass = 0;; ++pass) {
     if (pass > 64) return 2;  // pathological mesh: band not bounded
     for (size_t k = 0; k < tiles.size(); ++k)
-      for (int v : tiles[k]) home[v] = (int)k;
-    done.assign(tiles.size(), Done());
-    std::vector<char> ok(tiles.size(), 1);
+      for (int v : tiles[k].by[0]) home[v] = (int)k;
+    std::vector<size_t> todo;
+    for (size_t k = 0; k < tiles.size(); ++k)
+      if (!built[k]) todo.push_back(k);
     std::atomic<size_t> next{0};
-    auto work = [&]() {
-      Ctx W;
-      W.p = points;
-      W.tri_cols = tri_cols;
-      W.star_ptr = &star_ptr;
-      W.star_tri = &star_tri;
-      W.home = &home;
-      W.band = band;
-      W.group = group;
-      W.local.assign(n, 0);
-      W.lstamp.assign(n, 0);
-      W.seen.assign(nt, 0);
-      for (size_t i; (i = next.fetch_add(1)) < tiles.size();) ok[i] = build_tile(W, (int)i, tiles[i], done[i]);
+    auto work = [&](int w) {
+      Ctx& W = ctx[w];
+      if (W.local.empty()) {
+        W.local.assign(n, 0);
+        W.lstamp.assign(n, 0);
+        W.seen.assign(nt, 0);
+      }
+      for (size_t i; (i = next.fetch_add(1)) < todo.size();) {
+        const size_t k = todo[i];
+        done[k] = Done();
+        ok[k] = build_tile(W, (int)k, tiles[k], done[k]);
+        built[k] = 1;
+      }
     };
     std::vector<std::thread> pool;
-    for (int w = 1; w < std::min<int>(nw, (int)tiles.size()); ++w) pool.emplace_back(work);
-    work();
+    for (int w = 1; w < std::min<int>(nw, (int)todo.size()); ++w) pool.emplace_back(work, w);
+    work(0);
     for (auto& th : pool) th.join();
     if (std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; })) break;
-    // halve every failing tile across its sweep direction, in place
-    std::vector<std::vector<int>> next_tiles;
+    std::vector<Tile> nt_tiles;
+    std::vector<Done> nt_done;
+    std::vector<char> nt_built, nt_ok;
     for (size_t k = 0; k < tiles.size(); ++k) {
-      if (ok[k] || tiles[k].size() <= 1) {
-        if (!ok[k]) return 2;
-        next_tiles.push_back(std::move(tiles[k]));
+      if (ok[k]) {
+        nt_tiles.push_back(std::move(tiles[k]));
+        nt_done.push_back(std::move(done[k]));
+        nt_built.push_back(1);
+        nt_ok.push_back(1);
         continue;
       }
-      std::vector<int>& cols = tiles[k];
-      sort_along(points, cols, longest_axis(points, cols, 1));
-      const size_t h = cols.size() / 2;
-      next_tiles.emplace_back(cols.begin(), cols.begin() + h);
-      next_tiles.emplace_back(cols.begin() + h, cols.end());
+      if (tiles[k].size() <= 1) return 2;
+      cut(nt_tiles, tiles[k]);
+      for (int i = 0; i < 2; ++i) {
+        nt_done.emplace_back();
+        nt_built.push_back(0);
+        nt_ok.push_back(0);
+      }
     }
-    tiles.swap(next_tiles);
+    tiles.swap(nt_tiles);
+    done.swap(nt_done);
+    built.swap(nt_built);
+    ok.swap(nt_ok);
   }
+  // each tile's owned columns in sweep order
+  std::vector<std::vector<int>> owned(tiles.size());
+  for (size_t k = 0; k < tiles.size(); ++k) owned[k] = tiles[k].by[longest_axis(points, tiles[k])];
   Tiling* T = new Tiling();
   // halo slots in tile order; hl[v] = (slot, producer) of every halo copy of
   // column v, producers ascending
@@ -306,11 +487,18 @@ int hvb_tiling_build(const double* points, int n, const int* tri_cols, int nt, i
   T->lptr.assign(1, 0);
   T->xptr.assign(1, 0);
   T->pptr.assign(1, 0);
+  {
+    size_t ne = 0;
+    for (const Done& d : done) ne += d.ent_tri.size();
+    T->ent_tri.reserve(ne);
+    T->ent_meta.reserve(5 * ne);
+    T->perm.reserve(n);
+  }
   int c0 = 0;
   for (size_t k = 0; k < tiles.size(); ++k) {
     T->col0.push_back(c0);
     for (int pass2 = 0; pass2 < 2; ++pass2)
-      for (int v : tiles[k])
+      for (int v : owned[k])
         if (hl[v].empty() == (pass2 == 0)) {
           dev[v] = c0++;
           T->perm.push_back(v);
@@ -340,7 +528,7 @@ int hvb_tiling_build(const double* points, int n, const int* tri_cols, int nt, i
     // exchange entries of the receiving columns, device order: partial
     // first, then the halo copies by producer; and the distinct producers
     std::vector<int> prods;
-    for (int v : tiles[k]) {
+    for (int v : owned[k]) {
       if (hl[v].empty()) continue;
       T->xent.insert(T->xent.end(), {pslot[v], dev[v], 1, 0});
       for (size_t i = 0; i < hl[v].size(); ++i) {
