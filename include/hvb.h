@@ -103,7 +103,9 @@ int hvb_panel_data(const double* circumcenters, const double* radii, int nt, dou
  * [row_begin, row_begin+n_rows).  hats (HOST pointer) = nq x 3 hat values
  * hat_c(q) of the regular rule.  Non-regular, non-singular pairs are
  * appended to near_list as (row-list index, triangle).  Schedule arrays
- * from hvb_tiling_fetch (device copies; xent as int4).  A column local to
+ * from hvb_tiling_fetch (device copies; xent as int4); tile_order (device,
+ * n_tiles, or NULL = identity) is the launch order of the tiles -- longest
+ * first shortens the launch's last wave.  A column local to
  * several tiles is summed in a fixed order: every tile leaves its raw sums
  * of such a column in a slot of `halo`; whichever CTA (same rows) is the
  * last of the owner and its producers to finish adds the owner's partial
@@ -111,7 +113,8 @@ int hvb_panel_data(const double* circumcenters, const double* radii, int nt, dou
  * counters in `sched`; no CTA waits on another).
  * Replaces: row_pass1 regular part  assembly.py:170-200 and
  * _kernel_values 126-132 */
-int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_lptr,
+int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_order,
+                         const int* tile_lptr,
                          const int* lcol, const int* tile_xptr, const int* xent, const int* tile_pptr,
                          const int* prods, const int* tile_cptr, const int* cons, int n_tiles, int nq,
                          const double* hats, int row_begin, int n_rows, const double* rowdata, const int* row_col,

@@ -26,7 +26,7 @@ SIGNATURES = {
     "hvb_build_stream": [_P, _I, _P, _D, _P, _P, _LL, _I, _I, _P, _P],
     "hvb_panel_data": [_P, _P, _I, _D, _P, _P, _P, _P],
     "hvb_sweep_geometry": [_P],
-    "hvb_assemble_regular": [_P] * 10 + [_I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _LL, _P, _I, _P, _P, _P, _P, _LL, _P],
+    "hvb_assemble_regular": [_P] * 11 + [_I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _LL, _P, _I, _P, _P, _P, _P, _LL, _P],
     "hvb_assemble_singular": [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _I, _P],
     "hvb_charge_reduce": [_P, _I, _LL, _I, _P, _I, _P],
     "hvb_fill_float_cols": [_P, _P, _P, _I, _I, _I, _P],

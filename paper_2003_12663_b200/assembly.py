@@ -412,7 +412,7 @@ def _run_rows_on(dm, plan: RowPlan, A, counts: dict, part_ld: int = 0):
                                     device=dev)
                 _lib.call(
                     "hvb_assemble_regular", _lib.ptr(dm.stream_for(mode)), _lib.ptr(dm.tile_ptr),
-                    _lib.ptr(dm.tile_lptr), _lib.ptr(dm.lcol), _lib.ptr(dm.tile_xptr), _lib.ptr(dm.xent),
+                    _lib.ptr(dm.tile_order), _lib.ptr(dm.tile_lptr), _lib.ptr(dm.lcol), _lib.ptr(dm.tile_xptr), _lib.ptr(dm.xent),
                     _lib.ptr(dm.tile_pptr), _lib.ptr(dm.prods), _lib.ptr(dm.tile_cptr), _lib.ptr(dm.cons),
                     dm.n_tiles, dm.nq, hats, a, b - a, _lib.ptr(plan.rowdata), _lib.ptr(plan.col),
                     _lib.ptr(plan.scale), _lib.ptr(plan.out), _lib.ptr(A), part_ld, _lib.ptr(dm.tri_cols), mode,

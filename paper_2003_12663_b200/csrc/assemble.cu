@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
   }
   __syncthreads();
   const int nrb = gridDim.x;
-  const int rb = blockIdx.x, tile = blockIdx.y;
+  const int rb = blockIdx.x, tile = a.tile_order ? a.tile_order[blockIdx.y] : (int)blockIdx.y;
   const int cta_row0 = rb * (WPC * ROWS);
   const int live_warps = min(WPC, (a.n_rows - cta_row0 + ROWS - 1) / ROWS);
   const int64_t e0 = a.tile_ptr[tile], e1 = a.tile_ptr[tile + 1];

@@ -68,7 +68,8 @@ int hvb_sweep_geometry(int* out) {
 
 long long hvb_sweep_sched_ints(int n_rows, int n_tiles) { return (long long)hvb::sweep_sched_ints(n_rows, n_tiles); }
 
-int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_lptr,
+int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, const int* tile_order,
+                         const int* tile_lptr,
                          const int* lcol, const int* tile_xptr, const int* xent, const int* tile_pptr,
                          const int* prods, const int* tile_cptr, const int* cons, int n_tiles, int nq,
                          const double* hats, int row_begin, int n_rows, const double* rowdata, const int* row_col,
@@ -87,6 +88,7 @@ int hvb_assemble_regular(const double* panel_stream, const long long* tile_ptr, 
   a.tile_ptr = (const int64_t*)tile_ptr;
   if (!sched || !tile_lptr || !lcol || !tile_xptr || !tile_pptr || !tile_cptr)
     return fail(HVB_EARG, "hvb_assemble_regular: null schedule");
+  a.tile_order = tile_order;
   a.tile_lptr = tile_lptr;
   a.lcol = lcol;
   a.tile_xptr = tile_xptr;

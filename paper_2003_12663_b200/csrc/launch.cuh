@@ -10,6 +10,7 @@ namespace hvb {
 struct RegularArgs {
   const double* stream;     // tile panel streams (csrc/assemble.cu record formats)
   const int64_t* tile_ptr;  // (n_tiles+1) record offsets
+  const int* tile_order;    // launch order of the tiles (longest first), nullptr = identity
   const int* tile_lptr;     // (n_tiles+1) local column offsets
   const int* lcol;          // per local column: device column, or ~slot (halo copy / partial)
   const int* tile_xptr;     // (n_tiles+1) exchange entry offsets

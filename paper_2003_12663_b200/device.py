@@ -208,6 +208,8 @@ class DeviceMesh:
         self.perm = up(tiling.perm, **i32)
         self.col_dev = up(tiling.inv, **i32)
         self.tile_ptr = up(tiling.tile_ptr, dtype=torch.int64, device=device)
+        # launch order of the tiles: most records first (a shorter last wave)
+        self.tile_order = up(np.argsort(-np.diff(tiling.tile_ptr), kind="stable").astype(np.int32), **i32)
         self.tile_lptr = up(tiling.tile_lptr, **i32)
         self.lcol = up(tiling.lcol, **i32)
         self.tile_xptr = up(tiling.tile_xptr, **i32)
