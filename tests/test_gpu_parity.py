@@ -242,3 +242,28 @@ def test_regular_sweep_tiling_independent(cases, monkeypatch):
     b = assemble(m)[0].toarray()
     m._device_cache.clear()
     assert ora.entry_error(a, b) <= 5e-12  # the 2/r Newton step is accurate to 1.25e-12
+
+
+def test_regular_sweep_launch_chunks_bitwise(cases, monkeypatch):
+    """The halo exchange (csrc/tiling.cpp 5) does not depend on how the rows
+    are cut into launches: a scratch cap that forces one launch per 128 rows
+    (each with its own exchange slots and completion counters) gives the
+    same matrix bit for bit, with and without the longest-first tile order;
+    the exchange is exercised (several tiles, halo copies)."""
+    from paper_2003_12663_b200 import assembly, device
+
+    m = cases("diel2")
+    m._device_cache.clear()
+    monkeypatch.setattr(device, "MAX_TILE", 96)  # many tiles: many halo copies and receiving columns
+    dm = device.device_mesh(m)
+    assert dm.n_tiles > 2 and dm.tiling.n_halo > 0
+    a = assembly.assemble(m)[0].toarray()
+    m._device_cache.clear()
+    monkeypatch.setattr(assembly, "HALO_BYTES", 8 * 128 * device.device_mesh(m).n_slots)
+    b = assembly.assemble(m)[0].toarray()
+    np.testing.assert_array_equal(a, b)
+    m._device_cache.clear()
+    dm = device.device_mesh(m)
+    dm.tile_order = None
+    np.testing.assert_array_equal(a, assembly.assemble(m)[0].toarray())
+    m._device_cache.clear()
