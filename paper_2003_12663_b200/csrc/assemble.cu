@@ -170,11 +170,19 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
   // slot r / 32 + r, element 32: never touched by the sums), read by the
   // flush as shared-memory broadcasts instead of four shuffles per row
   // (branch-free stores + these: 237.5 -> 231.6 ms at cfg4)
-  static_assert(WIN >= 64 && STRIDE == 33, "row data lives in the pads of window slots 0..63");
+  constexpr bool PADS = WIN >= 64 && STRIDE == 33;  // else: shuffles
   __syncwarp();
-  win[lane * STRIDE + 32] = __longlong_as_double((long long)fout);
-  win[(32 + lane) * STRIDE + 32] = fscale;
+  if (PADS) {
+    win[lane * STRIDE + 32] = __longlong_as_double((long long)fout);
+    win[(32 + lane) * STRIDE + 32] = fscale;
+  }
   __syncwarp();
+  auto row_off = [&](int row) -> int64_t {
+    return PADS ? __double_as_longlong(win[row * STRIDE + 32]) : __shfl_sync(0xffffffffu, fout, row);
+  };
+  auto row_scale = [&](int row) -> double {
+    return PADS ? win[(32 + row) * STRIDE + 32] : __shfl_sync(0xffffffffu, fscale, row);
+  };
 
   int base = 0;
   // flush FLUSH finished columns: lane l writes rows (l / FLUSH) * FLUSH ..
@@ -195,8 +203,8 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
       for (int j = 0; j < FLUSH; ++j) {
         const int row = rh + j;
         const double v = wcol[row];
-        const int64_t off = __double_as_longlong(win[row * STRIDE + 32]);
-        sum = fma(v, win[(32 + row) * STRIDE + 32], sum);
+        const int64_t off = row_off(row);
+        sum = fma(v, row_scale(row), sum);
         if (dst < 0 && in && off >= 0) hcol[row] = v;
         wcol[row] = 0.0;
       }
@@ -211,8 +219,8 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
 #pragma unroll
       for (int j = 0; j < FLUSH; ++j) {
         const int row = rh + j;
-        const int64_t off = __double_as_longlong(win[row * STRIDE + 32]);
-        const double sc = win[(32 + row) * STRIDE + 32];
+        const int64_t off = row_off(row);
+        const double sc = row_scale(row);
         const double v = wcol[row];
         wcol[row] = 0.0;
         if (off >= 0 && in) colp[own ? off : row] = own ? v * sc : v;
