@@ -73,6 +73,17 @@ HVB_DEV double rinv3(double r2) {
   return (y * a) * p;
 }
 
+// r2^(-3/2) with the first-order correction only (5 FP64 ops, truncation
+// 15/8 e^2 ~ 4e-13 relative): point evaluations of E, whose parity bound is
+// 1e-8.  The tracer keeps rinv3 (its step decisions depend on E).
+HVB_DEV double rinv3_fast(double r2) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+  const double a = y * y;
+  const double e = __fma_rn(r2, a, -1.0);
+  return (y * a) * __fma_rn(e, -1.5, 1.0);
+}
+
 // 2/sqrt(r2): MUFU.RSQ64H seed + one Newton step with the 1/2 folded out,
 // y (3 - r2 y^2) -- 3 FP64 ops.  Callers scale their sums by 1/2 (or 1/8
 // for r^-3) at the end, which is exact.

@@ -38,7 +38,8 @@ constexpr int FCH = 32;   // panels per shared-memory chunk
 // chunk's regular panels summed in panel order into (sx, sy, sz) starting
 // from zero, non-regular (near) panels flagged / emitted.  src / cls / cols
 // point at the chunk's panel data (shared memory, or global memory in the
-// chunk-parallel mode).
+// chunk-parallel mode).  POT: 0 = E for the tracer (second-order r^-3,
+// rinv3), 1 = potential, 2 = E at points (first-order r^-3, rinv3_fast).
 template <int NQ, int POT>
 HVB_DEV void chunk_sum(const FieldArgs& a, d3 X, int own, bool live, int ti, int c0, int cn,
                        const double2* __restrict__ src, const double* __restrict__ cls, const int* __restrict__ cols,
@@ -60,10 +61,10 @@ HVB_DEV void chunk_sum(const FieldArgs& a, d3 X, int own, bool live, int ti, int
       const double2 p2q = src[(j * NQ + q) * 2 + 1];
       const double dx = X.x - p01.x, dy = X.y - p01.y, dz = X.z - p2q.x;
       const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      if (POT) {
+      if (POT == 1) {
         fx = fma(p2q.y, rsqrt_full(r2), fx);
       } else {
-        const double s = p2q.y * rinv3(r2);
+        const double s = p2q.y * (POT == 2 ? rinv3_fast(r2) : rinv3(r2));
         fx = fma(s, dx, fx);
         fy = fma(s, dy, fy);
         fz = fma(s, dz, fz);
@@ -361,7 +362,7 @@ static cudaError_t launch_field_nq(const FieldArgs& a, cudaStream_t st) {
   if (a.potential)
     k_field<NQ, 1><<<grid, FT, 0, st>>>(a);
   else
-    k_field<NQ, 0><<<grid, FT, 0, st>>>(a);
+    k_field<NQ, 2><<<grid, FT, 0, st>>>(a);  // E at points: first-order r^-3 (15 FP64 per node)
   return cudaGetLastError();
 }
 
