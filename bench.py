@@ -605,8 +605,15 @@ def run_b200(args):
     phases = []
     prof = []
     iters = 0
+    spans_all = os.environ.get("HVB_BENCH_SPANS")
     for k in range(args.steps):
-        ph, sol = one_step(prof if k == args.steps - 1 else None)
+        if spans_all:
+            prof = []
+        ph, sol = one_step(prof if (spans_all or k == args.steps - 1) else None)
+        if spans_all:
+            torch.cuda.synchronize(dev)
+            print(f"step {k}: phases {[round(x, 4) for x in ph]} spans "
+                  f"{[(lab, round(e0.elapsed_time(e1), 2)) for lab, e0, e1 in prof]}", file=sys.stderr)
         phases.append(ph)
         iters = sol.iterations
     t_end.record()
@@ -617,6 +624,9 @@ def run_b200(args):
     total = t_start.elapsed_time(t_end) / 1e3
     ph = np.array(phases).mean(axis=0)
     reg_t = sum(e0.elapsed_time(e1) for lab, e0, e1 in prof if lab == "regular") / 1e3
+    if os.environ.get("HVB_BENCH_SPANS"):  # dev: the last step's assembly spans
+        print("assembly spans (ms):", [(lab, round(e0.elapsed_time(e1), 2)) for lab, e0, e1 in prof],
+              "phases (s):", phases, file=sys.stderr)
     vec = torch.tensor([total, ph[0], ph[1], ph[2], ph[3], reg_t], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vec, op=dist.ReduceOp.MAX)

@@ -604,12 +604,22 @@ def assemble_rows(mesh: SurfaceMesh, dm, start: int, stop: int, precision: str =
     lda = -(-size // LDA_ALIGN) * LDA_ALIGN
     counts = {"near": 0}
     with torch.cuda.device(dev):
+        e0 = _mark()
         A = torch.empty((stop - start, lda), dtype=torch.float64, device=dev)
+        _span("alloc", e0)
         rows = np.arange(start, min(stop, n))
         if len(rows):
-            kind, scale, diag = _row_coeffs(mesh, rows)
+            e0 = _mark()
+            # the row plan is mesh-derived (rows, kinds, scales, output
+            # offsets): built and uploaded once per device mesh and row range
+            plans = dm.__dict__.setdefault("_plan_cache", {})
+            plan = plans.get((start, stop, lda))
             off = (rows - start) * lda
-            plan = _plan(dev, mesh.colloc_points[rows], mesh.colloc_normals[rows], kind, rows, scale, diag, off)
+            if plan is None:
+                kind, scale, diag = _row_coeffs(mesh, rows)
+                plan = _plan(dev, mesh.colloc_points[rows], mesh.colloc_normals[rows], kind, rows, scale, diag, off)
+                plans[(start, stop, lda)] = plan
+            _span("plan", e0)
             _run_rows(dm, plan, A, counts)
             global LAST_NEAR_ROWS
             LAST_NEAR_ROWS = np.zeros(n, dtype=np.int64)
