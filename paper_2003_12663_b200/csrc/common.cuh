@@ -61,21 +61,10 @@ HVB_DEV double rsqrt_newton(double r2) {
   return __fma_rn(y * 0.5, e, y);
 }
 
-// r2^(-3/2) from the MUFU.RSQ64H seed y0 in 6 FP64 ops: with a = y0^2 and
-// e = r2 a - 1 (|e| ~ 2^-21), r^-3 = y0^3 (1+e)^(-3/2) ~ y0 a (1 - 3/2 e +
-// 15/8 e^2); truncation O(e^3) ~ 1e-19 relative (cf. rsqrt_full cubed: 8 ops).
-HVB_DEV double rinv3(double r2) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
-  const double a = y * y;
-  const double e = __fma_rn(r2, a, -1.0);
-  const double p = __fma_rn(e, __fma_rn(e, 1.875, -1.5), 1.0);
-  return (y * a) * p;
-}
-
-// r2^(-3/2) with the first-order correction only (5 FP64 ops, truncation
-// 15/8 e^2 ~ 4e-13 relative): point evaluations of E, whose parity bound is
-// 1e-8.  The tracer keeps rinv3 (its step decisions depend on E).
+// r2^(-3/2) from the MUFU.RSQ64H seed y0 in 5 FP64 ops: with a = y0^2 and
+// e = r2 a - 1 (|e| ~ 2^-21), r^-3 = y0 a (1+e)^(-3/2) ~ y0 a (1 - 3/2 e);
+// truncation 15/8 e^2 ~ 4e-13 relative (the second-order term would cost a
+// sixth op for 1e-19).
 HVB_DEV double rinv3_fast(double r2) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
