@@ -612,13 +612,17 @@ def assemble_rows(mesh: SurfaceMesh, dm, start: int, stop: int, precision: str =
             e0 = _mark()
             # the row plan is mesh-derived (rows, kinds, scales, output
             # offsets): built and uploaded once per device mesh and row range
+            # (re-checked against the mesh's current row coefficients: a
+            # changed permittivity or potential rebuilds it)
             plans = dm.__dict__.setdefault("_plan_cache", {})
-            plan = plans.get((start, stop, lda))
+            kind, scale, diag = _row_coeffs(mesh, rows)
+            hit = plans.get((start, stop, lda))
             off = (rows - start) * lda
-            if plan is None:
-                kind, scale, diag = _row_coeffs(mesh, rows)
+            if hit is not None and all(np.array_equal(x, y) for x, y in zip(hit[1], (kind, scale, diag))):
+                plan = hit[0]
+            else:
                 plan = _plan(dev, mesh.colloc_points[rows], mesh.colloc_normals[rows], kind, rows, scale, diag, off)
-                plans[(start, stop, lda)] = plan
+                plans[(start, stop, lda)] = (plan, (kind, scale, diag))
             _span("plan", e0)
             _run_rows(dm, plan, A, counts)
             global LAST_NEAR_ROWS

@@ -267,3 +267,29 @@ def test_regular_sweep_launch_chunks_bitwise(cases, monkeypatch):
     dm.tile_order = None
     np.testing.assert_array_equal(a, assembly.assemble(m)[0].toarray())
     m._device_cache.clear()
+
+
+def test_row_plan_cache_follows_the_mesh(cases):
+    """assemble() keeps the uploaded row plan per device mesh; a changed row
+    coefficient (a dielectric row's permittivity) must rebuild it: the
+    re-assembly equals the assembly of a fresh mesh in the same state."""
+    from paper_2003_12663_b200.assembly import assemble
+
+    m = cases("diel2")
+    a0 = assemble(m)[0].toarray()
+    diel = np.flatnonzero(m.row_kind_code == 2)
+    assert len(diel)
+    saved = m.row_eps_plus.copy()
+    try:
+        m.row_eps_plus = saved.copy()
+        m.row_eps_plus[diel] *= 1.5
+        a1 = assemble(m)[0].toarray()
+        assert not np.array_equal(a0[diel], a1[diel])
+        from conftest import build_case
+
+        fresh = build_case("diel2")
+        fresh.row_eps_plus = m.row_eps_plus.copy()
+        np.testing.assert_array_equal(a1, assemble(fresh)[0].toarray())
+    finally:
+        m.row_eps_plus = saved
+        m._device_cache.clear()
