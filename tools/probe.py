@@ -29,7 +29,7 @@ del buf
 t = time.time(); mesh = F.rod_plane_mesh(scale); print(f"mesh nt={mesh.n_triangles} n={mesh.n_collocation} {time.time()-t:.1f}s")
 t = time.time()
 from paper_2003_12663_b200.device import device_mesh
-dm = device_mesh(mesh); torch.cuda.synchronize(); print(f"device mesh {time.time()-t:.1f}s tiles={dm.n_tiles} red={dm.tiling.redundancy:.3f} stream={dm.stream.numel()*8/1e6:.0f}MB")
+dm = device_mesh(mesh); torch.cuda.synchronize(); print(f"device mesh {time.time()-t:.1f}s tiles={dm.n_tiles} local/n={dm.tiling.redundancy:.3f} stream={dm.stream_for(0).numel()*8/1e6:.0f}MB")
 for rep in range(2):
     torch.cuda.synchronize(); t = time.time()
     A, rhs = assemble(mesh); torch.cuda.synchronize(); ta = time.time() - t
