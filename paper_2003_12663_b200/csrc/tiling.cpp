@@ -74,8 +74,8 @@ using Pts = const double*;
 // columns sorted along all three axes, so cutting it is a linear stable
 // partition and no tile is ever sorted again.
 // stable LSD radix sort of idx by coordinate ax rounded to float (the
-// order-preserving 32-bit image; 11-bit digits, digits shared by all keys
-// skipped; -0 == +0)
+// order-preserving 32-bit image; two 16-bit digits, a digit shared by all
+// keys skipped; -0 == +0)
 void radix_sort_along(Pts p, std::vector<int>& idx, int ax) {
   const size_t m = idx.size();
   std::vector<uint32_t> key(m), key2(m);
@@ -87,20 +87,20 @@ void radix_sort_along(Pts p, std::vector<int>& idx, int ax) {
     std::memcpy(&b, &x, 4);
     key[i] = (b >> 31) ? ~b : (b | (1u << 31));
   }
-  constexpr int DIG = 11, NB = 1 << DIG;
-  std::vector<size_t> cnt(NB);
+  constexpr int DIG = 16, NB = 1 << DIG;
+  std::vector<uint32_t> cnt(NB);
   for (int sh = 0; sh < 32; sh += DIG) {
     std::fill(cnt.begin(), cnt.end(), 0);
     for (size_t i = 0; i < m; ++i) ++cnt[(key[i] >> sh) & (NB - 1)];
     if (*std::max_element(cnt.begin(), cnt.end()) == m) continue;  // one digit value: order unchanged
-    size_t run = 0;
+    uint32_t run = 0;
     for (int d = 0; d < NB; ++d) {
-      const size_t c = cnt[d];
+      const uint32_t c = cnt[d];
       cnt[d] = run;
       run += c;
     }
     for (size_t i = 0; i < m; ++i) {
-      const size_t o = cnt[(key[i] >> sh) & (NB - 1)]++;
+      const uint32_t o = cnt[(key[i] >> sh) & (NB - 1)]++;
       key2[o] = key[i];
       idx2[o] = idx[i];
     }
@@ -487,13 +487,7 @@ int hvb_tiling_build(const double* points, int n, const int* tri_cols, int nt, i
   T->lptr.assign(1, 0);
   T->xptr.assign(1, 0);
   T->pptr.assign(1, 0);
-  {
-    size_t ne = 0;
-    for (const Done& d : done) ne += d.ent_tri.size();
-    T->ent_tri.reserve(ne);
-    T->ent_meta.reserve(5 * ne);
-    T->perm.reserve(n);
-  }
+  T->perm.reserve(n);
   int c0 = 0;
   for (size_t k = 0; k < tiles.size(); ++k) {
     T->col0.push_back(c0);
@@ -506,11 +500,25 @@ int hvb_tiling_build(const double* points, int n, const int* tri_cols, int nt, i
         }
     T->width.push_back(c0 - T->col0.back());
     const Done& d = done[k];
-    T->ent_tri.insert(T->ent_tri.end(), d.ent_tri.begin(), d.ent_tri.end());
-    T->ent_meta.insert(T->ent_meta.end(), d.ent_meta.begin(), d.ent_meta.end());
-    T->ptr.push_back((long long)T->ent_tri.size());
+    T->ptr.push_back(T->ptr.back() + (long long)d.ent_tri.size());
     T->band = std::max(T->band, d.band);
     T->real += d.real;
+  }
+  // the records of all tiles, copied in parallel to their offsets
+  T->ent_tri.resize(T->ptr.back());
+  T->ent_meta.resize(5 * T->ptr.back());
+  {
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+      for (size_t k; (k = next.fetch_add(1)) < tiles.size();) {
+        std::copy(done[k].ent_tri.begin(), done[k].ent_tri.end(), T->ent_tri.begin() + T->ptr[k]);
+        std::copy(done[k].ent_meta.begin(), done[k].ent_meta.end(), T->ent_meta.begin() + 5 * T->ptr[k]);
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int w = 1; w < std::min<int>(nw, (int)tiles.size()); ++w) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
   }
   for (size_t k = 0; k < tiles.size(); ++k) {
     // local columns: device column, or ~slot (halo copy / partial)
