@@ -853,12 +853,13 @@ def run_b200(args):
                               "device RK45 tracer + streamer (air_demo.gas)"},
             "roofline": {"bound": "fp64", "kernel": "k_sweep", "achieved": achieved,
                          "peak": tflops_peak, "unit": "TFLOP/s", "frac": achieved / tflops_peak if tflops_peak else None,
-                         "traffic": _ncu_traffic("k_sweep"),
+                         "traffic": _ncu_traffic("k_sweep")[0], "traffic_detail": _ncu_traffic("k_sweep")[1],
                          "peak_burst": tflops_burst, "frac_of_burst": achieved / tflops_burst if tflops_burst else None,
                          "peak_source": "measured DFMA kernel on this GPU (hvb_bench_dfma), sustained: launches back "
                                         "to back for 3 s, rate of the second half (the sweep runs inside a multi-second "
                                         "step); burst (one 6 ms launch) beside it"},
-            "roofline_gemv": {"bound": "hbm", "kernel": "k_gemv_f64", "traffic": _ncu_traffic("k_gemv"), "achieved": gemv_bytes / t_gemv / 1e9,
+            "roofline_gemv": {"bound": "hbm", "kernel": "k_gemv_f64", "traffic": _ncu_traffic("k_gemv_f64_v4")[0],
+                              "traffic_detail": _ncu_traffic("k_gemv_f64_v4")[1], "achieved": gemv_bytes / t_gemv / 1e9,
                               "peak": read_gbs, "unit": "GB/s", "frac": gemv_bytes / t_gemv / 1e9 / read_gbs,
                               "frac_of_measured_copy": (gemv_bytes / t_gemv / 1e9 / copy_gbs) if copy_gbs else None,
                               "measured_copy_gbs": copy_gbs,
@@ -887,23 +888,28 @@ def _count_near(mesh, rows):
     return per[rows]
 
 
-def _ncu_traffic(kernel="k_assemble_dual"):
-    """dram read+write bytes of one launch from the newest committed ncu
-    full capture (profiles/rNN_ncu_traffic.json, tools/profile_summary.py)."""
+def _ncu_traffic(kernel):
+    """(dram read+write bytes of one launch, detail) from the newest
+    committed ncu full capture (profiles/rNN_ncu_traffic.json,
+    tools/profile_summary.py); (None, None) if there is none."""
     import glob
 
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic.json")))
     if not files:
-        return None
+        return None, None
     try:
         with open(files[-1]) as fh:
             rec = json.load(fh).get(kernel)
     except (OSError, ValueError):
-        return None
-    notes = {"k_assemble_row4": "one SL launch of the regular sweep (dominated by the matrix write)",
-             "k_gemv": "one cfg4 matvec (the 79 GB row-major block is read once)"}
-    return None if rec is None else {"bytes_per_launch": rec["bytes_per_launch"], "source": os.path.basename(files[-1]),
-                                     "note": notes.get(kernel, "")}
+        return None, None
+    if rec is None:
+        return None, None
+    notes = {"k_sweep": "one SL launch of the regular sweep: the 72 GB matrix write + the exchange slots "
+                        "written and read back",
+             "k_gemv_f64_v4": "one cfg4 matvec (the 79 GB row-major block is read once)"}
+    return rec["bytes_per_launch"], {"dram_read_bytes": rec.get("dram_read_bytes"),
+                                     "dram_write_bytes": rec.get("dram_write_bytes"),
+                                     "source": os.path.basename(files[-1]), "note": notes.get(kernel, "")}
 
 
 def main():
