@@ -35,13 +35,13 @@ int hvb_version(void);
  * Replaces: TriangleTables.__init__  assembly.py:78-103 */
 int hvb_build_table(const double* nodes6, int nt, int nq, const double* rule, double* table, void* stream);
 
-/* Pack the per-column-tile panel streams (one record per (tile, panel)
- * entry; hvb_stream_record_doubles(nq, mode) doubles each): nodes, then an
+/* Pack the per-column-tile panel streams (one record per panel, in its
+ * tile; hvb_stream_record_doubles(nq, mode) doubles each): nodes, then an
  * 8-double tail = cc, thr = fl(eta*R), squared classification bracket,
- * panel id, first owned column, window slots of the owned corners, flags.
- * ent_meta = (mfirst, l0, l1, l2, flags) per entry, l = local column of an
- * owned corner or -1; the record stores l % window (window = the dump slot
- * for -1).  mode 0 (SL stream): per node pair 10 doubles, per node
+ * panel id, first local column, window slots of the corners, flags.
+ * ent_meta = (mfirst, l0, l1, l2, flags) per entry, l = local column of a
+ * corner or -1 (dummy records); the record stores l % window (window = the
+ * dump slot for -1).  mode 0 (SL stream): per node pair 10 doubles, per node
  * Y = -2 s (y - cc), P = s |y - cc|^2, Q = s with s = (4 pi / jw)^2;
  * mode 1 (ADL stream): per node (y, jw hat_0..2 / 4 pi).
  * Replaces: the per-row classification setup and the sample tables of

@@ -8,8 +8,12 @@
 // shared-memory counter), so warps are not lock-stepped by CTA barriers and
 // drift up to S stages apart.  Every lane evaluates all R records of a stage
 // for its row (R independent FP64 chains), adds the three corner sums into
-// its row of a 48-column shared-memory window (record order: no atomics,
-// bitwise reproducible) and finished groups of 16 columns are flushed once.
+// its row of a WIN-column shared-memory window of the tile's local columns
+// (record order: no atomics, bitwise reproducible) and finished groups of
+// FLUSH columns are flushed once: owned columns to A, halo copies and the
+// partials of receiving columns to exchange slots, summed after the sweep
+// by the last CTA (of the owner and its producers, same rows) to finish
+// (csrc/tiling.cpp 5).
 //
 // Record formats (csrc/tables.cu k_build_stream):
 //  * SL (MODE 0): per node pair 10 doubles [Yx0 Yy0 | Yz0 P0 | Q0 Q1 | Yx1 Yy1
@@ -23,8 +27,8 @@
 //    expansion loses at most ~120 ulp of r2 (~3e-14 relative).
 //  * ADL (MODE 1): per node 6 doubles (y, w hat_0, w hat_1, w hat_2).
 // Both end in an 8-double tail: cc, fl(eta R), bracket lo/hi, panel id,
-// first owned column, window byte offsets of the 3 corners, flags.  Stages
-// are built by csrc/tiling.cpp: the owned corners of one stage are distinct
+// first local column, window byte offsets of the 3 corners, flags.  Stages
+// are built by csrc/tiling.cpp: the corners of one stage are distinct local
 // columns (short stages padded with dummy records), so a stage updates the
 // window with 12 independent read-modify-writes.
 #include <cstdint>
@@ -362,9 +366,9 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
         off += __popc(msk[j]);
       }
     }
-    // window update of the whole stage at once: the stage's owned corners are
-    // distinct columns (csrc/tiling.cpp), so the 12 read-modify-writes are
-    // independent; only the never-flushed dump column may collide
+    // window update of the whole stage at once: the stage's corners are
+    // distinct local columns (csrc/tiling.cpp), so the 12 read-modify-writes
+    // are independent; only the never-flushed dump column (dummies) may collide
     double wv[R][3];
     int offs[R][3];
 #pragma unroll

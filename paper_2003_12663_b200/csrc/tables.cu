@@ -96,7 +96,7 @@ __global__ void k_build_stream(const double* __restrict__ table, int nq,
                                int64_t ne, int mode, int rec, int window, int wstride, double* __restrict__ out) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= ne) return;
-  const int t = ent_tri[e];  // -1: dummy record padding a stage (no owned corner, never emits)
+  const int t = ent_tri[e];  // -1: dummy record padding a stage (dump slot, never emits)
   double* o = out + e * rec;
   if (t < 0) {
     for (int k = 0; k < rec - 2; ++k) o[k] = 0.0;
@@ -145,9 +145,9 @@ __global__ void k_build_stream(const double* __restrict__ table, int nq,
   m[0] = t < 0 ? 0 : t;
   m[1] = em[0];
   short* l = reinterpret_cast<short*>(m + 2);
-  // byte offset of each owned corner's window column (local column mod
-  // window, csrc/assemble.cu WSTRIDE doubles per column); the dump column
-  // (index window) for corners owned by another tile
+  // byte offset of each corner's window column (local column mod window,
+  // csrc/assemble.cu WSTRIDE doubles per column); the dump column (index
+  // window) for dummy records
   for (int c = 0; c < 3; ++c) l[c] = (short)((em[1 + c] >= 0 ? em[1 + c] % window : window) * wstride * 8);
   l[3] = (short)em[4];
 }
