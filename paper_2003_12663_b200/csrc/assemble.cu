@@ -402,14 +402,13 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
   // importing its halo copies.  The CTA that completes a tile's count (its
   // partials and all copies of its receiving columns written, same rows)
   // performs that tile's exchange -- nobody waits.
-  __shared__ int s_todo[64];
+  __shared__ int s_todo[32];
   __shared__ int s_ntodo;
   __threadfence();
   asm volatile("bar.sync 1, %0;" ::"r"(live_warps * 32) : "memory");
-  if (wib == 0) {
-    const int cb = a.tile_cptr[tile], nc = a.tile_cptr[tile + 1] - cb;
-    int nt = 0;
-    for (int i0 = 0; i0 <= nc; i0 += 32) {
+  const int cb = a.tile_cptr[tile], nc = a.tile_cptr[tile + 1] - cb;
+  for (int i0 = 0; i0 <= nc; i0 += 32) {  // this tile, then its consumers, 32 at a time
+    if (wib == 0) {
       const int i = i0 + lane;
       bool done = false;
       int t = 0;
@@ -421,51 +420,51 @@ __global__ void __launch_bounds__(32 * sweep::WPC, sweep::MINB) k_sweep(RegularA
         done = old == need - 1;
       }
       const unsigned m = __ballot_sync(0xffffffffu, done);
-      if (done) s_todo[min(63, nt + __popc(m & ((1u << lane) - 1u)))] = t;
-      nt += __popc(m);
+      if (done) s_todo[__popc(m & ((1u << lane) - 1u))] = t;
+      __threadfence();
+      if (lane == 0) s_ntodo = __popc(m);
     }
-    __threadfence();
-    if (lane == 0) s_ntodo = min(nt, 64);
-  }
-  asm volatile("bar.sync 1, %0;" ::"r"(live_warps * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(live_warps * 32) : "memory");
 
-  // exchange of tile t: every receiving column = its partial + the halo
-  // copies of earlier tiles (producer order), scaled and written once;
-  // lane = row, 32 slots loaded per round trip
-  const int ntodo = s_ntodo;
-  for (int k = 0; k < ntodo; ++k) {
-    const int t = s_todo[k];
-    const int xb = a.tile_xptr[t], xe = a.tile_xptr[t + 1];
-    double acc = 0.0;
-    for (int x0 = xb; x0 < xe; x0 += 32) {
-      const int nb = min(32, xe - x0);
-      const int4 mine = a.xent[x0 + min(lane, nb - 1)];  // lane j holds entry x0 + j
-      double h[32];
+    // exchange of tile t: every receiving column = its partial + the halo
+    // copies of earlier tiles (producer order), scaled and written once;
+    // lane = row, 32 slots loaded per round trip
+    const int ntodo = s_ntodo;
+    for (int k = 0; k < ntodo; ++k) {
+      const int t = s_todo[k];
+      const int xb = a.tile_xptr[t], xe = a.tile_xptr[t + 1];
+      double acc = 0.0;
+      for (int x0 = xb; x0 < xe; x0 += 32) {
+        const int nb = min(32, xe - x0);
+        const int4 mine = a.xent[x0 + min(lane, nb - 1)];  // lane j holds entry x0 + j
+        double h[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int slot = __shfl_sync(0xffffffffu, mine.x, j);
-        h[j] = (j < nb && live0) ? __ldcg(halo + (size_t)slot * a.n_rows + lane) : 0.0;
-      }
+        for (int j = 0; j < 32; ++j) {
+          const int slot = __shfl_sync(0xffffffffu, mine.x, j);
+          h[j] = (j < nb && live0) ? __ldcg(halo + (size_t)slot * a.n_rows + lane) : 0.0;
+        }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (j < nb) {  // warp-uniform
-          const int dcol = __shfl_sync(0xffffffffu, mine.y, j);
-          const int first = __shfl_sync(0xffffffffu, mine.z, j);
-          const int last = __shfl_sync(0xffffffffu, mine.w, j);
-          acc = first ? h[j] : acc + h[j];
-          if (last) {
-            if (RED) {
-              double v = acc * fscale;
+        for (int j = 0; j < 32; ++j) {
+          if (j < nb) {  // warp-uniform
+            const int dcol = __shfl_sync(0xffffffffu, mine.y, j);
+            const int first = __shfl_sync(0xffffffffu, mine.z, j);
+            const int last = __shfl_sync(0xffffffffu, mine.w, j);
+            acc = first ? h[j] : acc + h[j];
+            if (last) {
+              if (RED) {
+                double v = acc * fscale;
 #pragma unroll
-              for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-              if (lane == 0) part[dcol] = v;
-            } else if (live0) {
-              a.A[fout + dcol] = acc * fscale;
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) part[dcol] = v;
+              } else if (live0) {
+                a.A[fout + dcol] = acc * fscale;
+              }
             }
           }
         }
       }
     }
+    asm volatile("bar.sync 1, %0;" ::"r"(live_warps * 32) : "memory");  // s_todo is rewritten next
   }
 }
 
