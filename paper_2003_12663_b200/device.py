@@ -241,6 +241,11 @@ class DeviceMesh:
             buf = self._slots = torch.empty(max(1, n_doubles), dtype=torch.float64, device=self.device)
         return buf
 
+    def release_scratch(self) -> None:
+        """Drop the kept exchange-slot scratch (it is re-made on the next
+        assembly); the memory returns to torch's caching allocator."""
+        self._slots = None
+
     def stream_for(self, mode: int):
         """Packed panel stream of the regular sweep: mode 0 (SL rows) or 1
         (ADL rows) record format (csrc/assemble.cu)."""
