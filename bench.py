@@ -603,17 +603,12 @@ def run_b200(args):
     barrier()
     t_start.record()
     phases = []
-    prof = []
+    step_spans = []  # every timed step's assembly spans (CUDA events on the launching stream)
     iters = 0
-    spans_all = os.environ.get("HVB_BENCH_SPANS")
     for k in range(args.steps):
-        if spans_all:
-            prof = []
-        ph, sol = one_step(prof if (spans_all or k == args.steps - 1) else None)
-        if spans_all:
-            torch.cuda.synchronize(dev)
-            print(f"step {k}: phases {[round(x, 4) for x in ph]} spans "
-                  f"{[(lab, round(e0.elapsed_time(e1), 2)) for lab, e0, e1 in prof]}", file=sys.stderr)
+        prof = []
+        ph, sol = one_step(prof)
+        step_spans.append(prof)
         phases.append(ph)
         iters = sol.iterations
     t_end.record()
@@ -623,10 +618,14 @@ def run_b200(args):
     launches = counter["n"]
     total = t_start.elapsed_time(t_end) / 1e3
     ph = np.array(phases).mean(axis=0)
-    reg_t = sum(e0.elapsed_time(e1) for lab, e0, e1 in prof if lab == "regular") / 1e3
-    if os.environ.get("HVB_BENCH_SPANS"):  # dev: the last step's assembly spans
-        print("assembly spans (ms):", [(lab, round(e0.elapsed_time(e1), 2)) for lab, e0, e1 in prof],
-              "phases (s):", phases, file=sys.stderr)
+    # the regular sweep's average time per step over the timed region (its
+    # SL + ADL launches), for the roofline
+    reg_steps = [sum(e0.elapsed_time(e1) for lab, e0, e1 in sp if lab == "regular") / 1e3 for sp in step_spans]
+    reg_t = float(np.mean(reg_steps))
+    if os.environ.get("HVB_BENCH_SPANS"):  # dev: per-step phases and assembly spans
+        for k, sp in enumerate(step_spans):
+            print(f"step {k}: phases {[round(x, 4) for x in phases[k]]} spans "
+                  f"{[(lab, round(e0.elapsed_time(e1), 2)) for lab, e0, e1 in sp]}", file=sys.stderr)
     vec = torch.tensor([total, ph[0], ph[1], ph[2], ph[3], reg_t], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vec, op=dist.ReduceOp.MAX)
@@ -855,6 +854,7 @@ def run_b200(args):
                          "peak": tflops_peak, "unit": "TFLOP/s", "frac": achieved / tflops_peak if tflops_peak else None,
                          "traffic": _ncu_traffic("k_sweep")[0], "traffic_detail": _ncu_traffic("k_sweep")[1],
                          "peak_burst": tflops_burst, "frac_of_burst": achieved / tflops_burst if tflops_burst else None,
+                         "kernel_s_per_step": [round(x, 5) for x in reg_steps],
                          "peak_source": "measured DFMA kernel on this GPU (hvb_bench_dfma), sustained: launches back "
                                         "to back for 3 s, rate of the second half (the sweep runs inside a multi-second "
                                         "step); burst (one 6 ms launch) beside it"},
